@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200-native sketched-EI operator pass (arXiv 2411.05771).
+
+Metric (BASELINE.json): "sketched EI operator passes/s at 512^2, 360->90 angles; % HBM/gather
+roofline".  One step = one whole pass of SURVEY §8(a) (a1 draw, a2 rotate, a3 two forward
+projections, a4 ramp, a5 FBP backprojection, a7 residuals, a8 gradient backprojection) over
+one batch of config 3 (512x512 fp32, B = 16, 360 angles, 725 bins, m = 90 uniform sketch,
+P = 2048), inputs resident in HBM, L2 flushed (256 MB write) before every timed step, each
+step timed with CUDA events on the launching stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl skei|reference]
+
+Multi-GPU (torchrun, one rank per GPU): the path partitions by image batch, so every rank
+runs its own config-3 batch (weak scaling, no data-path collective); value = N*K passes /
+max-over-ranks device time.  `--impl reference` times the fp64 oracle (the only reference
+this paper-only tier has) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "sketched EI operator passes/s at 512², 360→90 angles; % HBM/gather roofline"
+UNIT = "passes/s"
+STAGES = ["rotate", "radon_fwd_x2", "ramp", "residual_mc", "radon_adj_x2", "residual_ei"]
+LAUNCHES_PER_STEP = 9  # draw, rotate, fwd, ramp, mc partial+final, adj, ei partial+final
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
+    ap.add_argument("--mode", default="uniform", choices=["uniform", "interleaved"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, mode):
+    return {
+        "workload": f"{cfg.name}: {cfg.N}x{cfg.N} fp32 batch {cfg.B}, {cfg.n_full} angles, "
+                    f"{cfg.n_det} bins, sketch m={cfg.m} ({mode}), ramp FFT P={cfg.fft_len}, "
+                    f"{'per-image' if cfg.per_image_draws else 'per-pass shared'} draws",
+        "phantom": f"{cfg.K} random ellipses ({cfg.phantom}), seeded",
+        "noise": f"sigma = {cfg.noise} max|y| Gaussian",
+        "images_per_gpu": cfg.B,
+        "l2": "flushed (256 MB write) before every timed step",
+    }
+
+
+# ------------------------------------------------------------------ work counts
+def taps_per_pass(cfg):
+    """SURVEY §8(d)/App. A.6: taps = B (4 N^2 + 8 m N^2) (rotate 4/px; 2 fwd + 2 adj, 2 taps
+    per (pixel, angle))."""
+    return cfg.B * (4 * cfg.N ** 2 + 8 * cfg.m * cfg.N ** 2)
+
+
+def hbm_bytes_per_pass(cfg):
+    """Compulsory HBM bytes of the C-ABI call sequence: B (32 N^2 + 36 m n_det) (App. A.6)."""
+    return cfg.B * (32 * cfg.N ** 2 + 36 * cfg.m * cfg.n_det)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(cfg, seconds, mode, seed=0):
+    """Time the fp64 oracle (as it stands, single-threaded) on whole images of the workload
+    until ~`seconds` of CPU work; returns (passes/s, images, elapsed)."""
+    import oracle
+    x1, y = synth.make_workload(cfg, seed, images=range(1))
+    md = 1 if mode == "uniform" else 0
+    g, idx = oracle.draw(seed, 0, oracle.SHARED_IMAGE, cfg.n_full, cfg.m, md)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        oracle.sketched_pass(x1[0], y[0], g, idx, cfg.n_full)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or el / n * (n + 1) > 1.5 * seconds:
+            break
+    return (n / cfg.B) / el, n, el
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = synth.CONFIGS[args.config]
+    x1, y = synth.make_workload(cfg, args.seed, images=range(1))
+    md = 1 if args.mode == "uniform" else 0
+    times = []
+    for i in range(args.warmup + args.steps):
+        g, idx = oracle.draw(args.seed, i, oracle.SHARED_IMAGE, cfg.n_full, cfg.m, md)
+        t0 = time.perf_counter()
+        oracle.sketched_pass(x1[0], y[0], g, idx, cfg.n_full)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    per_image = float(np.mean(times))
+    value = 1.0 / (per_image * cfg.B)
+    sample = f"each step = the full pass on 1 of the {cfg.B} images of a {cfg.name} batch (1/{cfg.B} pass)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_image * cfg.B * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_desc(cfg, args.mode),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_05771_b200 as sk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = synth.CONFIGS[args.config]
+    mode = sk.MODE_UNIFORM if args.mode == "uniform" else sk.MODE_INTERLEAVED
+    shared = not cfg.per_image_draws
+    B, m, N = cfg.B, cfg.m, cfg.N
+    plan = sk.Plan.get(N, cfg.n_det, cfg.n_full, cfg.fft_len, device=local)
+
+    # inputs: this rank's images (global indices rank*B ...), resident in HBM
+    x1_np, y_np = synth.make_workload(cfg, args.seed, images=range(rank * B, (rank + 1) * B))
+    x1 = torch.from_numpy(x1_np).to(dev)
+    y = torch.from_numpy(y_np).to(dev)
+    out = sk.alloc_pass_outputs(plan, B, m, dev)
+    ws = plan.workspace(B, m)
+    gbuf = torch.empty(1 if shared else B, dtype=torch.int32, device=dev)
+    ibuf = torch.empty(1 if shared else B, m, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(it, events):
+        sk.draw_device(args.seed, it, rank * B, 1 if shared else B, shared, cfg.n_full, m, mode,
+                       g=gbuf, idx=ibuf)
+        sk.sketched_pass_profiled(plan, x1, y, gbuf, ibuf, events, out, ws)
+
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for i in range(args.warmup):
+        step(i * world + rank, [mk() for _ in range(7)])
+    torch.cuda.synchronize()
+
+    # shared-memory bandwidth probe (roofline denominator of the gather kernels)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.empty(2 * nsm, device=dev)
+    sk.smem_probe(2 * nsm, 50, sink)
+    e0, e1 = mk(), mk()
+    e0.record()
+    sk.smem_probe(2 * nsm, 1000, sink)
+    e1.record()
+    torch.cuda.synchronize()
+    probe_gbs = 2 * nsm * 1024 * 16 * 32 * 1000 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    recs = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev_start, ev_end = mk(), mk()
+            evs = [mk() for _ in range(7)]
+            ev_start.record(stream)
+            step((args.warmup + i) * world + rank, evs)
+            ev_end.record(stream)
+            recs.append((ev_start, evs, ev_end))
+        torch.cuda.synchronize()
+    step_ms = np.array([a.elapsed_time(c) for a, _, c in recs])
+    stage_ms = np.array([[evs[j].elapsed_time(evs[j + 1]) for j in range(6)] for _, evs, _ in recs])
+    draw_ms = np.array([a.elapsed_time(evs[0]) for a, evs, _ in recs])
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * args.steps / (total_ms * 1e-3)
+
+    # ---- end to end through the public host-buffer call (skei_pass_host)
+    e2e = None
+    if not args.no_e2e:
+        hx1 = torch.from_numpy(x1_np).pin_memory()
+        hy = torch.from_numpy(y_np).pin_memory()
+        hg = torch.empty(1 if shared else B, dtype=torch.int32).pin_memory()
+        hidx = torch.empty(1 if shared else B, m, dtype=torch.int32).pin_memory()
+        hmc = torch.empty(B).pin_memory()
+        hei = torch.empty(B).pin_memory()
+        d = dict(out)
+        d.update(x1=torch.empty_like(x1), y=torch.empty_like(y), g=torch.empty_like(gbuf),
+                 idx=torch.empty_like(ibuf))
+
+        def e2e_step(it):
+            for b in range(1 if shared else B):  # host draw (skei_draw)
+                gi, ii = sk.draw(args.seed, it, sk.SHARED_IMAGE if shared else rank * B + b,
+                                 cfg.n_full, m, mode)
+                hg[b] = gi
+                hidx[b] = torch.tensor(ii, dtype=torch.int32)
+            sk.sketched_pass_host(plan, hx1, hy, hg, hidx, d, hmc, hei, ws, x1)
+            torch.cuda.synchronize()
+            return float(hmc[0])
+
+        for i in range(2):
+            e2e_step(i)
+        el = 0.0
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step(1000 + i)
+            el += time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        h2d = hx1.numel() * 4 + hy.numel() * 4 + hg.numel() * 4 + hidx.numel() * 4
+        e2e = {"value": world * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(2 * B * 4), "timing": "host wall clock per step incl. host draw, "
+               "H2D from pinned memory, pass, D2H of mc/ei, stream sync"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (the two forward projections, one launch)
+    stage_mean = stage_ms.mean(axis=0)
+    dom = int(np.argmax(stage_mean))
+    sm_max = 1965.0
+    peak_theory = nsm * 128 * sm_max * 1e6 / 1e9  # GB/s: 148 SMs x 128 B/clk x 1965 MHz
+    peak = max(peak_theory, probe_gbs)
+    fwd_taps = 2 * B * 2 * m * N * N      # two projections, 2 taps per (pixel, angle)
+    adj_taps = 2 * B * 2 * m * N * N      # two backprojections
+    taps = {"radon_fwd_x2": fwd_taps, "radon_adj_x2": adj_taps}
+    dname = STAGES[dom]
+    if dname not in taps:
+        dname = "radon_fwd_x2" if stage_mean[1] >= stage_mean[4] else "radon_adj_x2"
+        dom = STAGES.index(dname)
+    achieved = 4.0 * taps[dname] / (stage_mean[dom] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dname)
+        except Exception:
+            traffic = None
+    t_gather = 4.0 * taps_per_pass(cfg) / (peak * 1e9)
+    t_hbm = hbm_bytes_per_pass(cfg) / (6548.8e9)
+    pass_frac = max(t_gather, t_hbm) / (ms_per_step * 1e-3)
+    roofline = {
+        "bound": "smem", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic,
+        "peak_source": f"max(theoretical {nsm} SMs x 128 B/clk x {sm_max:.0f} MHz = {peak_theory:.0f}, "
+                       f"live LDS.128 probe = {probe_gbs:.0f}) GB/s; MEASURED_PEAKS.json has no shared-memory figure",
+        "algorithmic": f"4 B per tap, {taps[dname]:.4g} taps per launch",
+        "pass_frac": pass_frac,
+        "pass_roofline": f"max(T_gather = 4 B x {taps_per_pass(cfg):.4g} taps / peak, T_hbm = "
+                         f"{hbm_bytes_per_pass(cfg):.4g} B / 6548.8 GB/s) / measured step time",
+    }
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        v, nimg, el = oracle_sample(cfg, args.cpu_seconds, args.mode, args.seed)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{nimg} image(s) of a {cfg.name} batch through the fp64 oracle pass "
+                         f"({el:.1f} s; {cfg.B} images = 1 pass)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_desc(cfg, args.mode),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "clocks": clk.summary(),
+        "stages_ms": {**{"draw": float(draw_ms.mean())},
+                      **{s: float(v) for s, v in zip(STAGES, stage_mean)}},
+        "images_per_s": value * B,
+        "taps_per_s": taps_per_pass(cfg) * value,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

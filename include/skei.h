@@ -1,0 +1,227 @@
+/*
+ * skei.h — C ABI of the B200-native sketched Equivariant Imaging operator pass
+ * (arXiv 2411.05771, "Sketched Equivariant Imaging").  PAPER.md references are
+ * lines of the paper's source; "R<n>" are the readings listed in DESIGN.md §2.
+ *
+ * The problem statement is y = A x + eps (Eq. 1) with A the
+ * parallel-beam Radon transform of sparse-view CT (L283) and A^+ its filtered
+ * backprojection (L40-L43, Eq. 2).  Sketched EI replaces A, A^+ by A_S := S A and
+ * A_S^+ with S an angle-subsampling operator (L92, §2.1; Eq. 6).  One
+ * iteration of Algorithm 1 (L117-L122) needs, besides the network:
+ *   draw (g, S) -> x2 = T_g x1 -> A_S x2, A_S x1 -> ramp -> A_S^+ A_S x2 ->
+ *   ||y_S - A_S x1||^2, ||x2 - x3||^2 -> 2 A_S^T (A_S x1 - y_S).
+ * Each step is one entry point below; skei_pass chains them.
+ *
+ * Conventions (all entry points):
+ *   - Tensors are fp32, C-contiguous, DEVICE pointers owned by the caller (e.g.
+ *     torch tensors) unless a parameter says "host".  The library never frees them.
+ *   - Image x      : [B][n][n], row r = 0 at the top, column c = 0 at the left;
+ *                    pixel centre (u, v) = (c - (n-1)/2, (n-1)/2 - r)        (R2)
+ *   - Sinogram p,y : [B][rows][n_det], angle-major; bin j at s_j = j - (n_det-1)/2,
+ *                    spacing 1 pixel                                          (R3)
+ *   - Angles       : int32 indices i into theta_i = i*pi/n_full, measured
+ *                    counter-clockwise from +u (R2, R4).  A sketch is m strictly
+ *                    increasing indices in [0, n_full); idx_stride = 0 shares one
+ *                    list across the batch, idx_stride = m gives image b the list
+ *                    at idx + b*m.  Index lists are trusted (not re-validated on
+ *                    the device).
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream), performs no device allocation and no hidden sync, and is
+ *     deterministic: no atomics, fixed reduction order, bitwise-repeatable.
+ *   - Arguments are validated on the host before any launch; a failing check
+ *     returns SKEI_ERR_SHAPE / SKEI_ERR_CONFIG / SKEI_ERR_ARG and launches nothing.
+ *     A launch failure returns SKEI_ERR_CUDA; asynchronous faults surface at the
+ *     caller's next synchronisation.
+ *   - A plan is immutable after creation and may be used from several streams and
+ *     threads concurrently (it owns only read-only device tables).
+ */
+#ifndef SKEI_H
+#define SKEI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SKEI_OK = 0,
+    SKEI_ERR_SHAPE = 1,     /* inconsistent sizes (SPEC-style "shape error")          */
+    SKEI_ERR_CONFIG = 2,    /* invalid configuration (m > n_full, bad fft_len, ...)   */
+    SKEI_ERR_ARG = 3,       /* NULL pointer / out-of-range scalar argument            */
+    SKEI_ERR_CUDA = 4,      /* a CUDA runtime call or kernel launch failed            */
+    SKEI_ERR_NO_DEVICE = 5  /* no usable sm_100 device                                */
+} skei_status;
+
+typedef void *skei_stream; /* cudaStream_t */
+
+/* Geometry of one CT system: n x n images, n_det detector bins, n_full angles on
+ * [0, pi).  fft_len = ramp FFT length P: a power of two >= 2*n_det - 1 (the length
+ * at which the zero-padded circular convolution equals the linear one, DESIGN.md
+ * §5 "ramp"); 0 selects the smallest such power of two.  Limits: 2 <= n <= 4096,
+ * 1 <= n_det <= 8192, 1 <= n_full <= 16384, P <= 16384. */
+typedef struct {
+    int32_t n;
+    int32_t n_det;
+    int32_t n_full;
+    int32_t fft_len;
+} skei_geometry;
+
+typedef struct skei_plan skei_plan; /* opaque */
+
+/* Builds the plan on `device`: fp64 trig table of the n_full angles, the ramp
+ * spectrum R[k] = DFT_P of the wrapped doubled Ram-Lak kernel (computed in fp64,
+ * stored fp32, pre-divided by P) and the FFT twiddles (fp64 -> fp32).  *out
+ * receives the plan (owned by the caller; release with skei_plan_destroy).
+ * Errors: SKEI_ERR_ARG (NULL), SKEI_ERR_CONFIG (limits above), SKEI_ERR_NO_DEVICE,
+ * SKEI_ERR_CUDA. */
+skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **out);
+void skei_plan_destroy(skei_plan *plan);                 /* NULL is a no-op */
+skei_status skei_plan_geometry(const skei_plan *plan, skei_geometry *out); /* resolved fft_len */
+const char *skei_status_string(skei_status status);     /* static string, never NULL */
+const char *skei_last_cuda_error(void);                  /* thread-local, after SKEI_ERR_CUDA */
+
+/* Device scratch needed by skei_fbp / skei_ei_residual / skei_pass for `batch`
+ * images and sketch size m (bytes; 256-byte aligned pieces). */
+size_t skei_workspace_bytes(const skei_plan *plan, int32_t batch, int32_t m);
+
+/* ---------------------------------------------------------------- a1: draws --
+ * Algorithm 1 step 2: sample g ~ G (|G| = 360 integer-degree
+ * rotations 1..360, L284) and a sketch S (L102: sample one of N predefined
+ * sketches; L299: interleaved minibatches).  Counter-based SplitMix64 keyed by
+ * (seed, stream, iter, image) — DESIGN.md §2 R5 gives the exact algorithm; the
+ * oracle implements it independently and the integers are bit-identical.
+ *   mode 0 = interleaved: requires n_full % m == 0; S = {b + k*n_full/m}.
+ *   mode 1 = uniform:     a uniformly random m-subset of [0, n_full), ascending.
+ *   image = UINT64_MAX    -> the per-pass shared draw, else a per-image draw.
+ * skei_draw is HOST code: g_deg (1 int) and angle_idx (m ints) are host pointers.
+ * Errors: SKEI_ERR_ARG (NULL), SKEI_ERR_CONFIG (m < 1, m > n_full, mode, divisibility). */
+skei_status skei_draw(uint64_t seed, uint64_t iter, uint64_t image, int32_t n_full,
+                      int32_t m, int32_t mode, int32_t *g_deg, int32_t *angle_idx);
+
+/* Same draws generated on the device for `count` images image0 .. image0+count-1
+ * (or, if shared != 0, the single shared draw: count must be 1): g_dev[count],
+ * idx_dev[count][m] are device pointers.  Bit-identical to skei_draw.
+ * Errors: as skei_draw; SKEI_ERR_CONFIG if n_full > 16384. */
+skei_status skei_draw_device(uint64_t seed, uint64_t iter, uint64_t image0, int32_t count,
+                             int32_t shared, int32_t n_full, int32_t m, int32_t mode,
+                             int32_t *g_dev, int32_t *idx_dev, skei_stream stream);
+
+/* ------------------------------------------------------------- a2: rotation --
+ * out = T_g x (x2 = T_g(x1); EI group action L65): bilinear
+ * interpolation about the image centre, zero outside the grid, content rotated
+ * counter-clockwise by g degrees; g in {90,180,270,360} are exact permutations
+ * (R11).  g_deg: device int32, one value (g_stride = 0) or one per image
+ * (g_stride = 1).  x, out: [B][n][n]; out must not alias x. */
+skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32_t B,
+                        const int32_t *g_deg, int32_t g_stride, skei_stream stream);
+
+/* ------------------------------------------------------ a3: forward A_S --------
+ * p[b][k][j] = sum_{r,c} x[b][r][c] * max(0, 1 - |u_c cos th + v_r sin th - s_j|),
+ * th = theta_{idx_b[k]} (BASELINE.json north_star projector; PAPER.md L283
+ * "discrete radon transform"; sketched rows L92 A_S := S A).  Computed as a
+ * gather per (angle, detector bin) — no atomics.  x: [B][n][n]; p: [B][m][n_det].
+ * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL,
+ * idx_stride not 0 or m). */
+skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int32_t B,
+                           const int32_t *idx, int32_t m, int32_t idx_stride,
+                           skei_stream stream);
+
+/* ---------------------------------------------------- a5/a8: adjoint A_S^T ------
+ * x[b] = scale * A_S^T p[b]: the exact transpose of skei_radon_fwd (linear
+ * interpolation of each sinogram row at t = u cos th + v sin th, out-of-range
+ * taps dropped), a per-pixel gather over the m angles.  p: [B][m][n_det];
+ * x: [B][n][n] (overwritten).  scale = 2 gives the MC-loss gradient
+ * 2 A_S^T r.  Errors as skei_radon_fwd. */
+skei_status skei_radon_adj(const skei_plan *plan, const float *p, float *x, int32_t B,
+                           const int32_t *idx, int32_t m, int32_t idx_stride, float scale,
+                           skei_stream stream);
+
+/* ------------------------------------------------------------- a4: ramp --------
+ * q[r] = h2 (*) p[r] for each of `rows` sinogram rows of length n_det: linear
+ * convolution with the doubled Ram-Lak kernel h2(0) = 1/2, h2(odd n) =
+ * -2/(pi^2 n^2), h2(even n != 0) = 0 (R8), computed as a zero-padded length-P
+ * complex FFT (two real rows per transform) x R[k] -> inverse FFT, truncated to
+ * n_det.  p, q: [rows][n_det]; q may alias p.  Errors: SKEI_ERR_SHAPE (rows < 1). */
+skei_status skei_ramp_filter(const skei_plan *plan, const float *p, float *q, int32_t rows,
+                             skei_stream stream);
+
+/* ------------------------------------------------------------ a4+a5: FBP -------
+ * x[b] = (pi / (2 m_total)) * A_S^T ramp(p[b])  — the sketched pseudo-inverse
+ * A_S^+ (BASELINE.json north_star; PAPER.md L92 A_S^+, L102 "FBP").  m_total is
+ * the sketch size the density compensation refers to (= m, or the full sketch
+ * size when the m angles are one rank's shard of an angle-split pass).  No
+ * circular mask (R10).  ws: >= skei_workspace_bytes(plan, B, m) bytes of device
+ * scratch.  Errors: as skei_radon_adj; SKEI_ERR_ARG if m_total < m. */
+skei_status skei_fbp(const skei_plan *plan, const float *p, float *x, int32_t B,
+                     const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
+                     void *ws, size_t ws_bytes, skei_stream stream);
+
+/* --------------------------------------------------------- a7: residuals -------
+ * r[b][k][j] = p1[b][k][j] - y[b][idx_b[k]][j];  mc[b] = sum r^2;
+ * ei[b] = sum (x2[b] - x3[b])^2  (PAPER.md L122 loss terms; Eq. 6;
+ * unnormalised squared l2 norms, R15).  p1: [B][m][n_det] (= A_S x1);
+ * y: [B][n_full][n_det] full measured sinogram; x2, x3: [B][n][n]; mc, ei: [B];
+ * r: [B][m][n_det] or NULL (not written).  Two-stage deterministic reduction.
+ * ws as skei_fbp. */
+skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float *y,
+                             const int32_t *idx, int32_t m, int32_t idx_stride,
+                             const float *x2, const float *x3, int32_t B,
+                             float *mc, float *ei, float *r,
+                             void *ws, size_t ws_bytes, skei_stream stream);
+
+/* ------------------------------------------------------ the whole pass (§8(a)) --
+ * One sketched-EI operator pass for B images given their draws (g, S):
+ *   x2 = T_g x1;  p2 = A_S x2;  p1 = A_S x1;  q = ramp(p2);
+ *   xfbp = (pi/2m) A_S^T q;  x3 = x3_in if non-NULL else xfbp (identity network,
+ *   R16);  r = p1 - y_S;  mc = ||r||^2;  ei = ||x2 - x3||^2;  grad = 2 A_S^T r.
+ * All outputs are required device buffers of the shapes above.  ws as skei_fbp
+ * (skei_workspace_bytes(plan, B, m)). */
+typedef struct {
+    float *x2, *p1, *p2, *q, *xfbp, *r, *grad, *mc, *ei;
+} skei_pass_outputs;
+
+skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                      const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                      int32_t idx_stride, const float *x3_in, const skei_pass_outputs *out,
+                      void *ws, size_t ws_bytes, skei_stream stream);
+
+/* End-to-end variant from HOST buffers: copies host x1 [B][n][n], host y
+ * [B][n_full][n_det], host g [B or 1] and host idx into the caller's device
+ * buffers (d_x1, d_y, d_g, d_idx, same shapes), runs skei_pass, and copies
+ * mc/ei back into host h_mc[B], h_ei[B].  Host buffers should be pinned for the
+ * copies to be asynchronous.  The caller synchronises `stream` before reading
+ * h_mc / h_ei. */
+skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
+                           const float *h_y, const int32_t *h_g, int32_t g_stride,
+                           const int32_t *h_idx, int32_t m, int32_t idx_stride,
+                           float *d_x1, float *d_y, int32_t *d_g, int32_t *d_idx,
+                           const skei_pass_outputs *out, float *h_mc, float *h_ei,
+                           void *ws, size_t ws_bytes, skei_stream stream);
+
+/* skei_pass with stage timing: `events` holds n_events (>= 7) cudaEvent_t handles
+ * created by the caller; event 0 is recorded before the first stage and event i after
+ * stage i of: 1 rotate, 2 forward (A_S x1 and A_S x2, one launch), 3 ramp,
+ * 4 residual r/mc, 5 the two backprojections (FBP and gradient, one launch),
+ * 6 residual ei.  Otherwise identical to skei_pass (same launches, same results). */
+skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1,
+                               const float *y, const int32_t *g_deg, int32_t g_stride,
+                               const int32_t *idx, int32_t m, int32_t idx_stride,
+                               const skei_pass_outputs *out, void *ws, size_t ws_bytes,
+                               void *const *events, int32_t n_events, skei_stream stream);
+
+/* Diagnostic: shared-memory read bandwidth probe (the roofline denominator of the
+ * gather kernels).  Launches `blocks` CTAs of 1024 threads that each
+ * stream LDS.128 over a 32 KB shared buffer `iters` times; `sink` (device, >= blocks
+ * floats) receives per-block checksums so the loads cannot be elided.  Bytes read =
+ * blocks * 1024 * 16 * 32 * iters. */
+skei_status skei_smem_probe(float *sink, int32_t blocks, int32_t iters, skei_stream stream);
+
+/* Library build info: "skei <version> sm_100a". */
+const char *skei_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKEI_H */

@@ -1,0 +1,330 @@
+"""paper_2411_05771_b200 — B200-native sketched Equivariant Imaging operator pass.
+
+Thin Python binding over the C ABI of include/skei.h (libskei.so, hand-written CUDA for
+sm_100a).  Argument marshalling only: every step of the pass runs in the library's
+kernels.  torch supplies device memory and the current CUDA stream.  There is no CPU
+fallback: if libskei.so is missing or no sm_100 device is present the calls raise.
+
+Names follow the C ABI (and the paper's notation, arXiv 2411.05771 Algorithm 1):
+    draw, draw_device        a1  (g, S) ~ G x sketches
+    rotate                   a2  x2 = T_g x1                       L120
+    radon_fwd                a3  A_S x                             L92, L283
+    ramp_filter              a4  Ram-Lak ramp (FFT)                L283 (iradon)
+    fbp                      a4+a5  A_S^+ = (pi/2m) A_S^T ramp     L92, L102
+    radon_adj                a5/a8  A_S^T p                        L122
+    ei_residual              a7  r, ||y_S - A_S x1||^2, ||x2-x3||^2  L122
+    sketched_pass            the whole pass (skei_pass)
+    sketched_pass_host       the whole pass from host buffers (skei_pass_host)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+__all__ = [
+    "Plan", "SkeiError", "lib", "lib_path", "draw", "draw_device", "rotate", "radon_fwd",
+    "radon_adj", "ramp_filter", "fbp", "ei_residual", "sketched_pass", "sketched_pass_host",
+    "sketched_pass_profiled", "smem_probe", "alloc_pass_outputs",
+    "workspace_bytes", "MODE_INTERLEAVED", "MODE_UNIFORM", "SHARED_IMAGE", "version",
+]
+
+MODE_INTERLEAVED, MODE_UNIFORM = 0, 1
+SHARED_IMAGE = (1 << 64) - 1
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libskei.so")
+_lib = None
+_lock = threading.Lock()
+
+
+class SkeiError(RuntimeError):
+    pass
+
+
+class _Geom(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("n_det", ctypes.c_int32), ("n_full", ctypes.c_int32),
+                ("fft_len", ctypes.c_int32)]
+
+
+class _PassOut(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad", "mc", "ei")]
+
+
+def lib():
+    """Load libskei.so (raises if the CUDA extension has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(lib_path):
+            raise SkeiError(f"CUDA extension missing: {lib_path} (run __graft_entry__.build())")
+        L = ctypes.CDLL(lib_path)
+        vp, i32, u64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_size_t
+        st = ctypes.c_int
+        sig = {
+            "skei_plan_create": ([ctypes.POINTER(_Geom), ctypes.c_int, ctypes.POINTER(vp)], st),
+            "skei_plan_destroy": ([vp], None),
+            "skei_plan_geometry": ([vp, ctypes.POINTER(_Geom)], st),
+            "skei_status_string": ([st], ctypes.c_char_p),
+            "skei_last_cuda_error": ([], ctypes.c_char_p),
+            "skei_workspace_bytes": ([vp, i32, i32], sz),
+            "skei_draw": ([u64, u64, u64, i32, i32, i32, vp, vp], st),
+            "skei_draw_device": ([u64, u64, u64, i32, i32, i32, i32, i32, vp, vp, vp], st),
+            "skei_rotate": ([vp, vp, vp, i32, vp, i32, vp], st),
+            "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp], st),
+            "skei_radon_adj": ([vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, vp], st),
+            "skei_ramp_filter": ([vp, vp, vp, i32, vp], st),
+            "skei_fbp": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
+            "skei_ei_residual": ([vp, vp, vp, vp, i32, i32, vp, vp, i32, vp, vp, vp, vp, sz, vp], st),
+            "skei_pass": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, ctypes.POINTER(_PassOut),
+                           vp, sz, vp], st),
+            "skei_pass_host": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp,
+                                ctypes.POINTER(_PassOut), vp, vp, vp, sz, vp], st),
+            "skei_pass_profiled": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.POINTER(_PassOut),
+                                    vp, sz, ctypes.POINTER(vp), i32, vp], st),
+            "skei_smem_probe": ([vp, i32, i32, vp], st),
+            "skei_version": ([], ctypes.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().skei_version().decode()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        msg = lib().skei_status_string(status).decode()
+        if status == 4:
+            msg += ": " + lib().skei_last_cuda_error().decode()
+        raise SkeiError(f"{what}: {msg} (status {status})")
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None, dtype=torch.float32, name="tensor"):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise SkeiError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise SkeiError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise SkeiError(f"{name}: expected a contiguous tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """skei_plan: immutable geometry tables on one device (fp64 trig, ramp spectrum, twiddles)."""
+
+    _cache: dict = {}
+
+    def __init__(self, n: int, n_det: int, n_full: int, fft_len: int = 0, device: int | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        g = _Geom(n, n_det, n_full, fft_len)
+        h = ctypes.c_void_p()
+        _check(lib().skei_plan_create(ctypes.byref(g), int(device), ctypes.byref(h)), "skei_plan_create")
+        self._h = h
+        out = _Geom()
+        _check(lib().skei_plan_geometry(h, ctypes.byref(out)), "skei_plan_geometry")
+        self.n, self.n_det, self.n_full, self.fft_len = out.n, out.n_det, out.n_full, out.fft_len
+        self.device = int(device)
+
+    @classmethod
+    def get(cls, n, n_det, n_full, fft_len=0, device=None):
+        if device is None:
+            device = torch.cuda.current_device()
+        key = (n, n_det, n_full, fft_len, device)
+        if key not in cls._cache:
+            cls._cache[key] = cls(n, n_det, n_full, fft_len, device)
+        return cls._cache[key]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            try:
+                _lib.skei_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def workspace(self, B: int, m: int) -> torch.Tensor:
+        nbytes = workspace_bytes(self, B, m)
+        return torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+
+def workspace_bytes(plan: Plan, B: int, m: int) -> int:
+    return int(lib().skei_workspace_bytes(plan.handle, B, m))
+
+
+def draw(seed: int, it: int, image: int, n_full: int, m: int, mode: int = MODE_UNIFORM):
+    """Host draw (skei_draw): returns (g_deg, list of m ascending angle indices)."""
+    g = ctypes.c_int32(0)
+    idx = (ctypes.c_int32 * m)()
+    _check(lib().skei_draw(seed, it, image, n_full, m, mode, ctypes.byref(g), idx), "skei_draw")
+    return g.value, list(idx)
+
+
+def draw_device(seed: int, it: int, image0: int, count: int, shared: bool, n_full: int, m: int,
+                mode: int = MODE_UNIFORM, g: torch.Tensor | None = None,
+                idx: torch.Tensor | None = None, device=None):
+    """Device draws (skei_draw_device) into int32 tensors g[count], idx[count, m]."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if g is None:
+        g = torch.empty(count, dtype=torch.int32, device=dev)
+    if idx is None:
+        idx = torch.empty(count, m, dtype=torch.int32, device=dev)
+    _check(lib().skei_draw_device(seed, it, image0, count, int(bool(shared)), n_full, m, mode,
+                                  _ptr(g, torch.int32, "g"), _ptr(idx, torch.int32, "idx"), _stream(g)),
+           "skei_draw_device")
+    return g, idx
+
+
+def _idx_stride(idx: torch.Tensor, B: int, m: int) -> int:
+    if idx.dim() == 1 or idx.shape[0] == 1:
+        return 0
+    if idx.shape[0] != B:
+        raise SkeiError(f"idx: expected [m] or [B, m], got {tuple(idx.shape)}")
+    return m
+
+
+def rotate(plan: Plan, x: torch.Tensor, g: torch.Tensor, out: torch.Tensor | None = None):
+    B = x.shape[0]
+    out = torch.empty_like(x) if out is None else out
+    g_stride = 0 if g.numel() == 1 else 1
+    _check(lib().skei_rotate(plan.handle, _ptr(x, name="x"), _ptr(out, name="out"), B,
+                             _ptr(g, torch.int32, "g"), g_stride, _stream(x)), "skei_rotate")
+    return out
+
+
+def radon_fwd(plan: Plan, x: torch.Tensor, idx: torch.Tensor, out: torch.Tensor | None = None):
+    B, m = x.shape[0], idx.shape[-1]
+    p = torch.empty(B, m, plan.n_det, dtype=torch.float32, device=x.device) if out is None else out
+    _check(lib().skei_radon_fwd(plan.handle, _ptr(x, name="x"), _ptr(p, name="p"), B,
+                                _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m), _stream(x)),
+           "skei_radon_fwd")
+    return p
+
+
+def radon_adj(plan: Plan, p: torch.Tensor, idx: torch.Tensor, scale: float = 1.0,
+              out: torch.Tensor | None = None):
+    B, m = p.shape[0], p.shape[1]
+    x = torch.empty(B, plan.n, plan.n, dtype=torch.float32, device=p.device) if out is None else out
+    _check(lib().skei_radon_adj(plan.handle, _ptr(p, name="p"), _ptr(x, name="x"), B,
+                                _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                ctypes.c_float(scale), _stream(p)), "skei_radon_adj")
+    return x
+
+
+def ramp_filter(plan: Plan, p: torch.Tensor, out: torch.Tensor | None = None):
+    rows = p.numel() // plan.n_det
+    q = torch.empty_like(p) if out is None else out
+    _check(lib().skei_ramp_filter(plan.handle, _ptr(p, name="p"), _ptr(q, name="q"), rows, _stream(p)),
+           "skei_ramp_filter")
+    return q
+
+
+def fbp(plan: Plan, p: torch.Tensor, idx: torch.Tensor, m_total: int | None = None,
+        out: torch.Tensor | None = None, ws: torch.Tensor | None = None):
+    B, m = p.shape[0], p.shape[1]
+    x = torch.empty(B, plan.n, plan.n, dtype=torch.float32, device=p.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    _check(lib().skei_fbp(plan.handle, _ptr(p, name="p"), _ptr(x, name="x"), B,
+                          _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m), int(m_total or m),
+                          _ptr(ws, torch.uint8, "ws"), ws.numel(), _stream(p)), "skei_fbp")
+    return x
+
+
+def ei_residual(plan: Plan, p1, y, idx, x2, x3, r: torch.Tensor | None = None, want_r: bool = True,
+                ws: torch.Tensor | None = None):
+    B, m = p1.shape[0], p1.shape[1]
+    mc = torch.empty(B, dtype=torch.float32, device=p1.device)
+    ei = torch.empty(B, dtype=torch.float32, device=p1.device)
+    if want_r and r is None:
+        r = torch.empty_like(p1)
+    ws = plan.workspace(B, m) if ws is None else ws
+    _check(lib().skei_ei_residual(plan.handle, _ptr(p1, name="p1"), _ptr(y, name="y"),
+                                  _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                  _ptr(x2, name="x2"), _ptr(x3, name="x3"), B, _ptr(mc), _ptr(ei),
+                                  _ptr(r) if want_r else None, _ptr(ws, torch.uint8, "ws"),
+                                  ws.numel(), _stream(p1)), "skei_ei_residual")
+    return mc, ei, r
+
+
+def alloc_pass_outputs(plan: Plan, B: int, m: int, device) -> dict:
+    f = dict(dtype=torch.float32, device=device)
+    img = (B, plan.n, plan.n)
+    sino = (B, m, plan.n_det)
+    return {"x2": torch.empty(img, **f), "p1": torch.empty(sino, **f), "p2": torch.empty(sino, **f),
+            "q": torch.empty(sino, **f), "xfbp": torch.empty(img, **f), "r": torch.empty(sino, **f),
+            "grad": torch.empty(img, **f), "mc": torch.empty(B, **f), "ei": torch.empty(B, **f)}
+
+
+def _pass_out(o: dict) -> _PassOut:
+    return _PassOut(*[ctypes.c_void_p(o[k].data_ptr()) for k in
+                      ("x2", "p1", "p2", "q", "xfbp", "r", "grad", "mc", "ei")])
+
+
+def sketched_pass(plan: Plan, x1, y, g, idx, x3=None, out: dict | None = None,
+                  ws: torch.Tensor | None = None):
+    """skei_pass: the whole sketched-EI operator pass.  Returns the dict of outputs."""
+    B, m = x1.shape[0], idx.shape[-1]
+    out = alloc_pass_outputs(plan, B, m, x1.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    po = _pass_out(out)
+    _check(lib().skei_pass(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
+                           _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,
+                           _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                           _ptr(x3, name="x3"), ctypes.byref(po), _ptr(ws, torch.uint8, "ws"),
+                           ws.numel(), _stream(x1)), "skei_pass")
+    return out
+
+
+def sketched_pass_profiled(plan: Plan, x1, y, g, idx, events, out: dict, ws: torch.Tensor):
+    """skei_pass_profiled: skei_pass with 7 caller-owned torch.cuda.Events recorded around
+    its 6 stages (rotate, forward x2, ramp, residual mc, backprojection x2, residual ei)."""
+    B, m = x1.shape[0], idx.shape[-1]
+    po = _pass_out(out)
+    ev = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    _check(lib().skei_pass_profiled(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
+                                    _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,
+                                    _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                    ctypes.byref(po), _ptr(ws, torch.uint8, "ws"), ws.numel(), ev,
+                                    len(events), _stream(x1)), "skei_pass_profiled")
+    return out
+
+
+def smem_probe(blocks: int, iters: int, sink: torch.Tensor):
+    """skei_smem_probe (diagnostic): shared-memory read bandwidth; bytes = blocks*1024*16*32*iters."""
+    _check(lib().skei_smem_probe(_ptr(sink, name="sink"), blocks, iters, _stream(sink)), "skei_smem_probe")
+
+
+def sketched_pass_host(plan: Plan, h_x1, h_y, h_g, h_idx, d: dict, h_mc, h_ei, ws, stream_tensor):
+    """skei_pass_host: H2D of (x1, y, g, idx) from (pinned) host tensors into d['x1'], d['y'],
+    d['g'], d['idx'], the pass, and D2H of mc/ei into h_mc/h_ei (asynchronous)."""
+    B, m = h_x1.shape[0], h_idx.shape[-1]
+    po = _pass_out(d)
+    g_stride = 0 if h_g.numel() == 1 else 1
+    idx_stride = 0 if (h_idx.dim() == 1 or h_idx.shape[0] == 1) else m
+    hp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _check(lib().skei_pass_host(plan.handle, B, hp(h_x1), hp(h_y), hp(h_g), g_stride, hp(h_idx), m,
+                                idx_stride, hp(d["x1"]), hp(d["y"]), hp(d["g"]), hp(d["idx"]),
+                                ctypes.byref(po), hp(h_mc), hp(h_ei), hp(ws), ws.numel(),
+                                _stream(stream_tensor)), "skei_pass_host")

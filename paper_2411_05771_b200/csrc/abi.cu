@@ -1,0 +1,389 @@
+// abi.cu — the extern "C" entry points of include/skei.h: host-side validation,
+// plan tables, workspace sizing and the pass orchestration.  Every numeric step runs
+// in the kernels of the sibling .cu files.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+using namespace skei;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+skei_status cuda_fail(cudaError_t e) {
+    std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e));
+    return SKEI_ERR_CUDA;
+}
+
+#define SKEI_CUDA(call)                        \
+    do {                                       \
+        cudaError_t e_ = (call);               \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+// Scoped device switch: the library must not change the caller's current device.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+double ramlak2(long n) {  // doubled Ram-Lak kernel h2 (R8)
+    if (n == 0) return 0.5;
+    if (n % 2 == 0) return 0.0;
+    return -2.0 / (M_PI * M_PI * (double)n * (double)n);
+}
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+skei_status check_idx_args(const skei_plan *plan, int B, const int32_t *idx, int m,
+                           int idx_stride) {
+    if (!plan || !idx) return SKEI_ERR_ARG;
+    if (B < 1 || m < 1 || m > plan->n_full) return SKEI_ERR_SHAPE;
+    if (idx_stride != 0 && idx_stride != m) return SKEI_ERR_ARG;
+    return SKEI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *skei_version(void) { return "skei 0.1 sm_100a"; }
+
+const char *skei_status_string(skei_status s) {
+    switch (s) {
+        case SKEI_OK: return "ok";
+        case SKEI_ERR_SHAPE: return "shape error";
+        case SKEI_ERR_CONFIG: return "config error";
+        case SKEI_ERR_ARG: return "invalid argument";
+        case SKEI_ERR_CUDA: return "CUDA error";
+        case SKEI_ERR_NO_DEVICE: return "no usable sm_100 device";
+    }
+    return "unknown status";
+}
+
+const char *skei_last_cuda_error(void) { return g_cuda_err; }
+
+skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **out) {
+    if (!geom || !out) return SKEI_ERR_ARG;
+    *out = nullptr;
+    const int n = geom->n, n_det = geom->n_det, n_full = geom->n_full;
+    if (n < 2 || n > 4096 || n_det < 1 || n_det > 8192 || n_full < 1 || n_full > 16384)
+        return SKEI_ERR_CONFIG;
+    int P = geom->fft_len;
+    if (P == 0) {
+        P = 2;
+        while (P < 2 * n_det - 1) P *= 2;
+    }
+    if (!is_pow2(P) || P < 2 * n_det - 1 || P > 16384 || P < 4) return SKEI_ERR_CONFIG;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return SKEI_ERR_NO_DEVICE;
+    DeviceGuard guard(device);
+    if (!guard.ok) return SKEI_ERR_NO_DEVICE;
+    cudaDeviceProp prop;
+    SKEI_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return SKEI_ERR_NO_DEVICE;  // built for sm_100a only
+
+    // fp64 tables on the host
+    std::vector<double2> trig(n_full);
+    for (int i = 0; i < n_full; ++i) {
+        // theta_i = i*pi/n_full; exact values at 0 and pi/2
+        if (2 * i == n_full) {
+            trig[i] = make_double2(0.0, 1.0);
+        } else {
+            double th = M_PI * (double)i / (double)n_full;
+            trig[i] = make_double2(std::cos(th), std::sin(th));
+        }
+    }
+    std::vector<float> ramp(P);
+    {
+        // R[k] = sum_n h_P[n] cos(2 pi k n / P), h_P = h2 wrapped onto P points (even),
+        // = 1/2 + 2 sum_{odd l < P/2} h2(l) cos(2 pi k l / P); stored / P (inverse-FFT scale).
+        std::vector<double> R(P / 2 + 1);
+        for (int k = 0; k <= P / 2; ++k) {
+            double acc = 0.5;
+            for (int l = 1; l < P / 2; l += 2) {
+                long t = ((long)k * l) % P;
+                acc += 2.0 * ramlak2(l) * std::cos(2.0 * M_PI * (double)t / (double)P);
+            }
+            R[k] = acc;
+        }
+        for (int k = 0; k < P; ++k) ramp[k] = (float)(R[k <= P / 2 ? k : P - k] / (double)P);
+    }
+    std::vector<float2> tw(P / 2);
+    for (int k = 0; k < P / 2; ++k) {
+        double a = 2.0 * M_PI * (double)k / (double)P;
+        tw[k] = make_float2((float)std::cos(a), (float)(-std::sin(a)));
+    }
+
+    skei_plan *p = new skei_plan();
+    p->device = device;
+    p->n = n;
+    p->n_det = n_det;
+    p->n_full = n_full;
+    p->fft_len = P;
+    p->log2_fft = 0;
+    while ((1 << p->log2_fft) < P) ++p->log2_fft;
+    p->num_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * n_full);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_ramp, sizeof(float) * P);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_tw, sizeof(float2) * (P / 2));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * n_full, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_ramp, ramp.data(), sizeof(float) * P, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * (P / 2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        skei_plan_destroy(p);
+        return cuda_fail(e);
+    }
+    *out = p;
+    return SKEI_OK;
+}
+
+void skei_plan_destroy(skei_plan *plan) {
+    if (!plan) return;
+    DeviceGuard guard(plan->device);
+    if (plan->d_trig) cudaFree(plan->d_trig);
+    if (plan->d_ramp) cudaFree(plan->d_ramp);
+    if (plan->d_tw) cudaFree(plan->d_tw);
+    delete plan;
+}
+
+skei_status skei_plan_geometry(const skei_plan *plan, skei_geometry *out) {
+    if (!plan || !out) return SKEI_ERR_ARG;
+    out->n = plan->n;
+    out->n_det = plan->n_det;
+    out->n_full = plan->n_full;
+    out->fft_len = plan->fft_len;
+    return SKEI_OK;
+}
+
+size_t skei_workspace_bytes(const skei_plan *plan, int32_t batch, int32_t m) {
+    if (!plan || batch < 1 || m < 1) return 0;
+    size_t q = align256(sizeof(float) * (size_t)batch * m * plan->n_det);
+    return q + align256(residual_ws_bytes(plan, batch, m));
+}
+
+skei_status skei_draw(uint64_t seed, uint64_t iter, uint64_t image, int32_t n_full, int32_t m,
+                      int32_t mode, int32_t *g_deg, int32_t *angle_idx) {
+    if (!g_deg || !angle_idx) return SKEI_ERR_ARG;
+    if (n_full < 1 || m < 1 || m > n_full) return SKEI_ERR_CONFIG;
+    if (mode != 0 && mode != 1) return SKEI_ERR_CONFIG;
+    if (mode == 0 && n_full % m != 0) return SKEI_ERR_CONFIG;
+    return host_draw(seed, iter, image, n_full, m, mode, g_deg, angle_idx) == 0
+               ? SKEI_OK
+               : SKEI_ERR_CONFIG;
+}
+
+skei_status skei_draw_device(uint64_t seed, uint64_t iter, uint64_t image0, int32_t count,
+                             int32_t shared, int32_t n_full, int32_t m, int32_t mode,
+                             int32_t *g_dev, int32_t *idx_dev, skei_stream stream) {
+    if (!g_dev || !idx_dev) return SKEI_ERR_ARG;
+    if (count < 1 || (shared && count != 1)) return SKEI_ERR_ARG;
+    if (n_full < 1 || n_full > 16384 || m < 1 || m > n_full) return SKEI_ERR_CONFIG;
+    if (mode != 0 && mode != 1) return SKEI_ERR_CONFIG;
+    if (mode == 0 && n_full % m != 0) return SKEI_ERR_CONFIG;
+    SKEI_CUDA(launch_draw(seed, iter, image0, count, shared, n_full, m, mode, g_dev, idx_dev,
+                          (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32_t B,
+                        const int32_t *g_deg, int32_t g_stride, skei_stream stream) {
+    if (!plan || !x || !out || !g_deg) return SKEI_ERR_ARG;
+    if (B < 1) return SKEI_ERR_SHAPE;
+    if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    if (x == out) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    SKEI_CUDA(launch_rotate(plan, x, out, B, g_deg, g_stride, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int32_t B,
+                           const int32_t *idx, int32_t m, int32_t idx_stride,
+                           skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x || !p) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    FwdJob job{x, p};
+    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_radon_adj(const skei_plan *plan, const float *p, float *x, int32_t B,
+                           const int32_t *idx, int32_t m, int32_t idx_stride, float scale,
+                           skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x || !p) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    AdjJob job{p, x, scale};
+    SKEI_CUDA(launch_radon_adj(plan, &job, 1, B, idx, m, idx_stride, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_ramp_filter(const skei_plan *plan, const float *p, float *q, int32_t rows,
+                             skei_stream stream) {
+    if (!plan || !p || !q) return SKEI_ERR_ARG;
+    if (rows < 1) return SKEI_ERR_SHAPE;
+    DeviceGuard guard(plan->device);
+    SKEI_CUDA(launch_ramp(plan, p, q, rows, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_fbp(const skei_plan *plan, const float *p, float *x, int32_t B,
+                     const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
+                     void *ws, size_t ws_bytes, skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x || !p || !ws) return SKEI_ERR_ARG;
+    if (m_total < m) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    float *q = (float *)ws;
+    cudaStream_t s = (cudaStream_t)stream;
+    SKEI_CUDA(launch_ramp(plan, p, q, B * m, s));
+    AdjJob job{q, x, (float)(M_PI / (2.0 * (double)m_total))};
+    SKEI_CUDA(launch_radon_adj(plan, &job, 1, B, idx, m, idx_stride, s));
+    return SKEI_OK;
+}
+
+skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float *y,
+                             const int32_t *idx, int32_t m, int32_t idx_stride,
+                             const float *x2, const float *x3, int32_t B, float *mc,
+                             float *ei, float *r, void *ws, size_t ws_bytes,
+                             skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!p1 || !y || !x2 || !x3 || !mc || !ei || !ws) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    char *w = (char *)ws + align256(sizeof(float) * (size_t)B * m * plan->n_det);
+    SKEI_CUDA(launch_residual(plan, p1, y, idx, m, idx_stride, x2, x3, B, mc, ei, r, w,
+                              (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+namespace {
+
+skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                     const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                     int32_t idx_stride, const float *x3_in, const skei_pass_outputs *o,
+                     void *ws, size_t ws_bytes, cudaEvent_t const *ev, cudaStream_t s) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x1 || !y || !g_deg || !o || !ws) return SKEI_ERR_ARG;
+    if (!o->x2 || !o->p1 || !o->p2 || !o->q || !o->xfbp || !o->r || !o->grad || !o->mc ||
+        !o->ei)
+        return SKEI_ERR_ARG;
+    if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    char *wres = (char *)ws + align256(sizeof(float) * (size_t)B * m * plan->n_det);
+    auto mark = [&](int i) -> cudaError_t { return ev ? cudaEventRecord(ev[i], s) : cudaSuccess; };
+    const float fbp_scale = (float)(M_PI / (2.0 * m));
+
+    SKEI_CUDA(mark(0));
+    // a2: x2 = T_g x1
+    SKEI_CUDA(launch_rotate(plan, x1, o->x2, B, g_deg, g_stride, s));
+    SKEI_CUDA(mark(1));
+    // a3: p1 = A_S x1 and p2 = A_S x2 in one launch
+    FwdJob fj[2] = {{x1, o->p1}, {o->x2, o->p2}};
+    SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, s));
+    SKEI_CUDA(mark(2));
+    // a4: q = ramp(p2)
+    SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s));
+    SKEI_CUDA(mark(3));
+    // a7 (MC part): r = p1 - y_S, mc
+    SKEI_CUDA(launch_residual(plan, o->p1, y, idx, m, idx_stride, nullptr, nullptr, B, o->mc,
+                              nullptr, o->r, wres, s));
+    SKEI_CUDA(mark(4));
+    // a5 + a8: xfbp = (pi/2m) A_S^T q and grad = 2 A_S^T r in one launch
+    AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale}, {o->r, o->grad, 2.0f}};
+    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s));
+    SKEI_CUDA(mark(5));
+    // a7 (EI part): ei = ||x2 - x3||^2, x3 = x3_in or the identity network's xfbp
+    SKEI_CUDA(launch_residual(plan, nullptr, nullptr, idx, m, idx_stride, o->x2,
+                              x3_in ? x3_in : o->xfbp, B, nullptr, o->ei, nullptr, wres, s));
+    SKEI_CUDA(mark(6));
+    return SKEI_OK;
+}
+
+}  // namespace
+
+skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                      const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                      int32_t idx_stride, const float *x3_in, const skei_pass_outputs *o,
+                      void *ws, size_t ws_bytes, skei_stream stream) {
+    return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, x3_in, o, ws, ws_bytes,
+                    nullptr, (cudaStream_t)stream);
+}
+
+skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1,
+                               const float *y, const int32_t *g_deg, int32_t g_stride,
+                               const int32_t *idx, int32_t m, int32_t idx_stride,
+                               const skei_pass_outputs *out, void *ws, size_t ws_bytes,
+                               void *const *events, int32_t n_events, skei_stream stream) {
+    if (!events || n_events < 7) return SKEI_ERR_ARG;
+    for (int i = 0; i < 7; ++i)
+        if (!events[i]) return SKEI_ERR_ARG;
+    return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, nullptr, out, ws,
+                    ws_bytes, (cudaEvent_t const *)events, (cudaStream_t)stream);
+}
+
+skei_status skei_smem_probe(float *sink, int32_t blocks, int32_t iters, skei_stream stream) {
+    if (!sink || blocks < 1 || iters < 1) return SKEI_ERR_ARG;
+    SKEI_CUDA(launch_smem_probe(sink, blocks, iters, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
+skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
+                           const float *h_y, const int32_t *h_g, int32_t g_stride,
+                           const int32_t *h_idx, int32_t m, int32_t idx_stride, float *d_x1,
+                           float *d_y, int32_t *d_g, int32_t *d_idx,
+                           const skei_pass_outputs *o, float *h_mc, float *h_ei, void *ws,
+                           size_t ws_bytes, skei_stream stream) {
+    if (!plan || !h_x1 || !h_y || !h_g || !h_idx || !d_x1 || !d_y || !d_g || !d_idx || !o ||
+        !h_mc || !h_ei)
+        return SKEI_ERR_ARG;
+    skei_status st = check_idx_args(plan, B, h_idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nn = (size_t)plan->n * plan->n, ny = (size_t)plan->n_full * plan->n_det;
+    SKEI_CUDA(cudaMemcpyAsync(d_x1, h_x1, sizeof(float) * B * nn, cudaMemcpyHostToDevice, s));
+    SKEI_CUDA(cudaMemcpyAsync(d_y, h_y, sizeof(float) * B * ny, cudaMemcpyHostToDevice, s));
+    SKEI_CUDA(cudaMemcpyAsync(d_g, h_g, sizeof(int32_t) * (g_stride ? B : 1),
+                              cudaMemcpyHostToDevice, s));
+    SKEI_CUDA(cudaMemcpyAsync(d_idx, h_idx, sizeof(int32_t) * (size_t)m * (idx_stride ? B : 1),
+                              cudaMemcpyHostToDevice, s));
+    st = skei_pass(plan, B, d_x1, d_y, d_g, g_stride, d_idx, m, idx_stride, nullptr, o, ws,
+                   ws_bytes, stream);
+    if (st != SKEI_OK) return st;
+    SKEI_CUDA(cudaMemcpyAsync(h_mc, o->mc, sizeof(float) * B, cudaMemcpyDeviceToHost, s));
+    SKEI_CUDA(cudaMemcpyAsync(h_ei, o->ei, sizeof(float) * B, cudaMemcpyDeviceToHost, s));
+    return SKEI_OK;
+}
+
+}  // extern "C"

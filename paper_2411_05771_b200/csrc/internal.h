@@ -1,0 +1,80 @@
+// internal.h — private declarations of the skei CUDA library (sm_100a).
+// Nothing here is part of the ABI (include/skei.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/skei.h"
+
+struct skei_plan {
+    int device;
+    int n, n_det, n_full, fft_len, log2_fft;
+    int num_sms;
+    double2 *d_trig;  // [n_full] (cos, sin) of theta_i = i*pi/n_full, fp64
+    float *d_ramp;    // [fft_len] R[k] / P, fp32 (from an fp64 DFT)
+    float2 *d_tw;     // [fft_len/2] exp(-2 pi i k / P), fp32 (from fp64)
+};
+
+namespace skei {
+
+// Kernel-facing geometry constants, passed by value.
+struct Geom {
+    int n, n_det, n_full;
+    double h;   // (n-1)/2
+    double hd;  // (n_det-1)/2
+    const double2 *trig;
+};
+
+inline Geom geom_of(const skei_plan *p) {
+    Geom g;
+    g.n = p->n;
+    g.n_det = p->n_det;
+    g.n_full = p->n_full;
+    g.h = (p->n - 1) * 0.5;
+    g.hd = (p->n_det - 1) * 0.5;
+    g.trig = p->d_trig;
+    return g;
+}
+
+// ---- launchers (return cudaGetLastError()) ----
+// Up to two independent (input, output) pairs share one launch (e.g. A_S x1 and A_S x2).
+struct FwdJob { const float *x; float *p; };
+cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
+                             const int32_t *idx, int m, int idx_stride, cudaStream_t s);
+
+struct AdjJob { const float *p; float *x; float scale; };
+cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
+                             const int32_t *idx, int m, int idx_stride, cudaStream_t s);
+
+cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
+                          const int32_t *g, int g_stride, cudaStream_t s);
+
+cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
+                        cudaStream_t s);
+
+// Residual: partials in ws (float2 per (image, chunk)), then final reduce.
+size_t residual_ws_bytes(const skei_plan *plan, int B, int m);
+cudaError_t launch_residual(const skei_plan *plan, const float *p1, const float *y,
+                            const int32_t *idx, int m, int idx_stride, const float *x2,
+                            const float *x3, int B, float *mc, float *ei, float *r,
+                            void *ws, cudaStream_t s);
+
+cudaError_t launch_draw(uint64_t seed, uint64_t iter, uint64_t image0, int count, int shared,
+                        int n_full, int m, int mode, int32_t *g, int32_t *idx, cudaStream_t s);
+
+cudaError_t launch_smem_probe(float *sink, int blocks, int iters, cudaStream_t s);
+
+// Host draw (library implementation of DESIGN.md R5).
+int host_draw(uint64_t seed, uint64_t iter, uint64_t image, int n_full, int m, int mode,
+              int32_t *g, int32_t *idx);
+
+// Batch grouping: images sharing one angle list are processed together in groups of bb.
+inline int pick_bb(int B, int idx_stride) {
+    if (idx_stride != 0) return 1;
+    if (B % 4 == 0) return 4;
+    if (B % 2 == 0) return 2;
+    return 1;
+}
+
+}  // namespace skei

@@ -16,3 +16,13 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_sessionstart(session):
+    """Build the in-tree CUDA library (nvcc cross-compiles without a GPU) and the oracle
+    if they are missing or stale, so every test sees the current sources."""
+    import oracle
+    from paper_2411_05771_b200 import build as _build
+
+    oracle.build()
+    _build.build()

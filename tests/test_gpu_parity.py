@@ -1,0 +1,268 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Bar (BASELINE.json north_star): max|gpu - ref| <= 1e-4 * max|ref| for every output tensor
+(sinograms, filtered sinograms, images, residuals, gradients), scalars within 1e-4
+relative, integer draws bit-identical.  Inputs are seeded synthetic workloads (synth/).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2411_05771_b200 as sk
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+SH = sk.SHARED_IMAGE
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def close(gpu, ref, name, tol=TOL):
+    g = gpu.detach().double().cpu().numpy() if torch.is_tensor(gpu) else np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert g.shape == ref.shape, (name, g.shape, ref.shape)
+    scale = float(np.abs(ref).max())
+    err = float(np.abs(g - ref).max())
+    assert err <= tol * scale + 1e-30, f"{name}: max|err| {err:.3e} > {tol:g} * max|ref| {scale:.3e}"
+    return err / max(scale, 1e-300)
+
+
+def dev(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def idx_t(idx):
+    return dev(np.asarray(idx, np.int32), torch.int32)
+
+
+# ------------------------------------------------------------------------------ draws
+@pytest.mark.parametrize("name", list(synth.CONFIGS))
+@pytest.mark.parametrize("mode", [sk.MODE_UNIFORM, sk.MODE_INTERLEAVED])
+def test_device_draws_bit_identical(name, mode):
+    cfg = synth.CONFIGS[name]
+    for it in (0, 1, 17):
+        g, idx = sk.draw_device(0, it, 0, 1, True, cfg.n_full, cfg.m, mode)
+        og, oidx = oracle.draw(0, it, SH, cfg.n_full, cfg.m, mode)
+        assert int(g[0]) == og and np.array_equal(idx[0].cpu().numpy(), oidx)
+        g, idx = sk.draw_device(0, it, 0, cfg.B, False, cfg.n_full, cfg.m, mode)
+        for b in range(cfg.B):
+            og, oidx = oracle.draw(0, it, b, cfg.n_full, cfg.m, mode)
+            assert int(g[b]) == og and np.array_equal(idx[b].cpu().numpy(), oidx)
+
+
+# --------------------------------------------------------------------- stage parity
+GEOMS = [  # (N, n_det, n_full, fft_len, B, m)
+    (64, 91, 32, 256, 2, 8),       # cfg1
+    (256, 363, 128, 1024, 8, 32),  # cfg2
+    (50, 71, 20, 0, 3, 5),         # ragged tile, odd batch (BB = 1)
+    (40, 57, 12, 0, 4, 12),        # m = n_full (full EI), BB = 4
+    (33, 47, 9, 0, 2, 1),          # odd N, single angle
+]
+
+
+def _plan(N, n_det, n_full, P):
+    return sk.Plan.get(N, n_det, n_full, P)
+
+
+@pytest.mark.parametrize("geom", GEOMS)
+def test_rotate_parity(geom):
+    N, n_det, n_full, P, B, m = geom
+    plan = _plan(N, n_det, n_full, P)
+    x = synth.rand_images(B, N, 1)
+    for g in (1, 37, 90, 123, 180, 270, 301, 360):
+        out = sk.rotate(plan, dev(x), idx_t([g]))
+        ref = oracle.rotate(x, g)
+        if g % 90 == 0:
+            assert np.array_equal(out.cpu().numpy(), np.rot90(x, g // 90, axes=(1, 2)))
+        close(out, ref, f"rotate g={g}")
+    gs = [(17 * b + 5) % 360 + 1 for b in range(B)]  # per-image g
+    out = sk.rotate(plan, dev(x), idx_t(gs))
+    for b in range(B):
+        close(out[b], oracle.rotate(x[b], gs[b]), f"rotate per-image b={b}")
+
+
+def _draw_list(n_full, m, seed=3):
+    return oracle.draw(seed, 0, SH, n_full, m)[1]
+
+
+@pytest.mark.parametrize("geom", GEOMS)
+def test_radon_fwd_parity(geom):
+    N, n_det, n_full, P, B, m = geom
+    plan = _plan(N, n_det, n_full, P)
+    x = synth.rand_images(B, N, 2)
+    idx = _draw_list(n_full, m)
+    p = sk.radon_fwd(plan, dev(x), idx_t(idx))
+    close(p, oracle.fwd(x, idx, n_full, n_det), "fwd")
+    # per-image sketches
+    idxs = np.stack([oracle.draw(5, 0, b, n_full, m)[1] for b in range(B)])
+    p = sk.radon_fwd(plan, dev(x), idx_t(idxs))
+    for b in range(B):
+        close(p[b], oracle.fwd(x[b], idxs[b], n_full, n_det), f"fwd per-image b={b}")
+
+
+@pytest.mark.parametrize("geom", GEOMS)
+def test_radon_adj_parity(geom):
+    N, n_det, n_full, P, B, m = geom
+    plan = _plan(N, n_det, n_full, P)
+    y = synth.rand_sinograms(B, m, n_det, 3)
+    idx = _draw_list(n_full, m)
+    x = sk.radon_adj(plan, dev(y), idx_t(idx), 2.0)
+    close(x, oracle.adj(y, idx, n_full, N, 2.0), "adj")
+    idxs = np.stack([oracle.draw(6, 0, b, n_full, m)[1] for b in range(B)])
+    x = sk.radon_adj(plan, dev(y), idx_t(idxs), 1.0)
+    for b in range(B):
+        close(x[b], oracle.adj(y[b], idxs[b], n_full, N), f"adj per-image b={b}")
+
+
+@pytest.mark.parametrize("n_det,P", [(91, 256), (363, 1024), (363, 2048), (725, 2048), (1449, 4096), (7, 16)])
+def test_ramp_parity(n_det, P):
+    plan = sk.Plan.get(max(2, n_det // 2), n_det, 8, P)
+    rows = 7  # odd row count: the last packed pair has one row
+    p = synth.rand_sinograms(1, rows, n_det, 4)[0]
+    q = sk.ramp_filter(plan, dev(p))
+    close(q, oracle.ramp(p), f"ramp n_det={n_det} P={P}")
+
+
+def test_ramp_fft_length_independent():
+    """Same result for P = 1024 and P = 2048 at n_det = 363 (App. A.1 exactness)."""
+    p = dev(synth.rand_sinograms(1, 6, 363, 5)[0])
+    a = sk.ramp_filter(sk.Plan.get(256, 363, 128, 1024), p)
+    b = sk.ramp_filter(sk.Plan.get(256, 363, 128, 2048), p)
+    close(a, b.double().cpu().numpy(), "P independence", tol=2e-6)
+
+
+@pytest.mark.parametrize("geom", GEOMS[:3])
+def test_fbp_parity(geom):
+    N, n_det, n_full, P, B, m = geom
+    plan = _plan(N, n_det, n_full, P)
+    y = synth.rand_sinograms(B, m, n_det, 7)
+    idx = _draw_list(n_full, m)
+    x = sk.fbp(plan, dev(y), idx_t(idx))
+    close(x, oracle.fbp(y, idx, n_full, N), "fbp")
+    x = sk.fbp(plan, dev(y), idx_t(idx), m_total=4 * m)  # angle-shard scaling pi/(2 m_total)
+    close(x, oracle.fbp(y, idx, n_full, N, m_total=4 * m), "fbp m_total")
+
+
+@pytest.mark.parametrize("geom", GEOMS[:3])
+def test_residual_parity(geom):
+    N, n_det, n_full, P, B, m = geom
+    plan = _plan(N, n_det, n_full, P)
+    rng = np.random.default_rng(9)
+    p1 = rng.standard_normal((B, m, n_det)).astype(np.float32)
+    y = rng.standard_normal((B, n_full, n_det)).astype(np.float32)
+    x2 = rng.standard_normal((B, N, N)).astype(np.float32)
+    x3 = rng.standard_normal((B, N, N)).astype(np.float32)
+    idx = _draw_list(n_full, m)
+    mc, ei, r = sk.ei_residual(plan, dev(p1), dev(y), idx_t(idx), dev(x2), dev(x3))
+    for b in range(B):
+        omc, oei, orr = oracle.residual(p1[b], y[b], idx, x2[b], x3[b])
+        close(r[b], orr, "r")
+        assert abs(float(mc[b]) - omc) <= TOL * omc
+        assert abs(float(ei[b]) - oei) <= TOL * oei
+    mc2, ei2, _ = sk.ei_residual(plan, dev(p1), dev(y), idx_t(idx), dev(x2), dev(x2), want_r=False)
+    assert torch.all(ei2 == 0)
+    assert torch.equal(mc, mc2)
+
+
+# ---------------------------------------------------------------------- whole pass
+def _check_pass(cfg, images, mode=sk.MODE_UNIFORM, it=0, seed=0):
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = synth.make_workload(cfg, seed)
+    shared = not cfg.per_image_draws
+    g, idx = sk.draw_device(seed, it, 0, 1 if shared else cfg.B, shared, cfg.n_full, cfg.m, mode)
+    out = sk.sketched_pass(plan, dev(x1), dev(y), g if not shared else g[:1], idx)
+    torch.cuda.synchronize()
+    worst = {}
+    for b in images:
+        og, oidx = oracle.draw(seed, it, SH if shared else b, cfg.n_full, cfg.m, mode)
+        gi = int(g[0 if shared else b])
+        assert gi == og and np.array_equal(idx[0 if shared else b].cpu().numpy(), oidx)
+        ref = oracle.sketched_pass(x1[b], y[b], og, oidx, cfg.n_full)
+        for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad"):
+            worst[k] = max(worst.get(k, 0), close(out[k][b], ref[k], f"{cfg.name} {k} b={b}"))
+        for k in ("mc", "ei"):
+            rel = abs(float(out[k][b]) - ref[k]) / abs(ref[k])
+            assert rel <= TOL, f"{cfg.name} {k} b={b}: rel err {rel:.2e}"
+            worst[k] = max(worst.get(k, 0), rel)
+    return out, worst
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("mode", [sk.MODE_UNIFORM, sk.MODE_INTERLEAVED])
+def test_pass_parity_small_configs(name, mode):
+    cfg = synth.CONFIGS[name]
+    _check_pass(cfg, range(cfg.B), mode)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_pass_parity_full_size(name):
+    """BASELINE.json's full sizes in the bench's launch configuration (whole batch on the
+    GPU); the oracle recomputes the first and last image of the batch in full."""
+    cfg = synth.CONFIGS[name]
+    _check_pass(cfg, sorted({0, cfg.B - 1}))
+
+
+def test_pass_deterministic_bitwise():
+    cfg = synth.CONFIGS["cfg2"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = synth.make_workload(cfg)
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    a = sk.sketched_pass(plan, dev(x1), dev(y), g, idx)
+    b = sk.sketched_pass(plan, dev(x1), dev(y), g, idx)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+
+
+def test_gpu_adjoint_identity():
+    cfg = synth.CONFIGS["cfg2"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x = synth.rand_images(2, cfg.N, 10)
+    yv = synth.rand_sinograms(2, cfg.m, cfg.n_det, 11)
+    idx = idx_t(_draw_list(cfg.n_full, cfg.m))
+    Ax = sk.radon_fwd(plan, dev(x), idx).double().cpu().numpy()
+    ATy = sk.radon_adj(plan, dev(yv), idx).double().cpu().numpy()
+    lhs, rhs = float((Ax * yv).sum()), float((x * ATy).sum())
+    assert abs(lhs - rhs) / (np.linalg.norm(Ax) * np.linalg.norm(yv)) <= 1e-6
+
+
+def test_pass_host_matches_device_pass():
+    cfg = synth.CONFIGS["cfg1"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = synth.make_workload(cfg)
+    g, idx = sk.draw(0, 0, SH, cfg.n_full, cfg.m)
+    ref = sk.sketched_pass(plan, dev(x1), dev(y), idx_t([g]), idx_t(idx))
+    h = {k: torch.from_numpy(v).pin_memory() for k, v in (("x1", x1), ("y", y))}
+    hg = torch.tensor([g], dtype=torch.int32).pin_memory()
+    hidx = torch.tensor(idx, dtype=torch.int32).pin_memory()
+    d = sk.alloc_pass_outputs(plan, cfg.B, cfg.m, "cuda")
+    d.update(x1=torch.empty_like(dev(x1)), y=torch.empty_like(dev(y)),
+             g=torch.empty(1, dtype=torch.int32, device="cuda"),
+             idx=torch.empty(cfg.m, dtype=torch.int32, device="cuda"))
+    hmc = torch.empty(cfg.B).pin_memory()
+    hei = torch.empty(cfg.B).pin_memory()
+    ws = plan.workspace(cfg.B, cfg.m)
+    sk.sketched_pass_host(plan, h["x1"], h["y"], hg, hidx, d, hmc, hei, ws, d["x2"])
+    torch.cuda.synchronize()
+    assert torch.equal(hmc, ref["mc"].cpu()) and torch.equal(hei, ref["ei"].cpu())
+    assert torch.equal(d["grad"], ref["grad"])
+
+
+def test_invalid_shapes_raise():
+    plan = sk.Plan.get(64, 91, 32, 256)
+    x = torch.zeros(0, 64, 64, device="cuda")
+    with pytest.raises(sk.SkeiError):
+        sk.radon_fwd(plan, x, idx_t([0, 1]))
+    with pytest.raises(sk.SkeiError):
+        sk.radon_fwd(plan, torch.zeros(1, 64, 64, device="cuda"), idx_t(list(range(33))))
+    with pytest.raises(sk.SkeiError):
+        sk.rotate(plan, torch.zeros(1, 64, 64, device="cuda", dtype=torch.float64), idx_t([3]))
