@@ -41,7 +41,7 @@ L2_FLUSH_BYTES = 256 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
@@ -62,6 +62,7 @@ def workload_desc(cfg, mode):
         "noise": f"sigma = {cfg.noise} max|y| Gaussian",
         "images_per_gpu": cfg.B,
         "l2": "flushed (256 MB write) before every timed step",
+        "launch": "one CUDA graph per step (draw + 8 pass kernels), replayed on the timed stream",
     }
 
 
@@ -104,7 +105,7 @@ class ClockSampler:
                 self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv is not None:
@@ -216,8 +217,28 @@ def main():
         sk.sketched_pass_profiled(plan, x1, y, gbuf, ibuf, events, out, ws)
 
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def mk_created():
+        e = mk()
+        e.record(stream)  # creates the cudaEvent_t outside any capture
+        return e
+
+    # Every step (draw a1 + pass a2..a8, 9 kernels) is captured once into its own CUDA graph
+    # (the draw's iteration index is a kernel argument); the stage events become external
+    # event-record nodes, so each replay records the per-stage boundaries.
+    n_iter = args.warmup + args.steps
+    step_events = [[mk_created() for _ in range(7)] for _ in range(n_iter)]
+    torch.cuda.synchronize()
+    graphs = []
+    cap = torch.cuda.Stream(dev)
+    for i in range(n_iter):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cap):
+            step(i * world + rank, step_events[i])
+        graphs.append(gr)
+    torch.cuda.synchronize()
     for i in range(args.warmup):
-        step(i * world + rank, [mk() for _ in range(7)])
+        graphs[i].replay()
     torch.cuda.synchronize()
 
     # shared-memory bandwidth probe (roofline denominator of the gather kernels)
@@ -239,11 +260,10 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             ev_start, ev_end = mk(), mk()
-            evs = [mk() for _ in range(7)]
             ev_start.record(stream)
-            step((args.warmup + i) * world + rank, evs)
+            graphs[args.warmup + i].replay()
             ev_end.record(stream)
-            recs.append((ev_start, evs, ev_end))
+            recs.append((ev_start, step_events[args.warmup + i], ev_end))
         torch.cuda.synchronize()
     step_ms = np.array([a.elapsed_time(c) for a, _, c in recs])
     stage_ms = np.array([[evs[j].elapsed_time(evs[j + 1]) for j in range(6)] for _, evs, _ in recs])

@@ -302,6 +302,9 @@ def sketched_pass_profiled(plan: Plan, x1, y, g, idx, events, out: dict, ws: tor
     its 6 stages (rotate, forward x2, ramp, residual mc, backprojection x2, residual ei)."""
     B, m = x1.shape[0], idx.shape[-1]
     po = _pass_out(out)
+    for e in events:  # torch creates the cudaEvent_t lazily, on its first record()
+        if e.cuda_event == 0:
+            e.record()
     ev = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
     _check(lib().skei_pass_profiled(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
                                     _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,

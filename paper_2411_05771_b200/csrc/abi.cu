@@ -300,7 +300,17 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
     char *wres = (char *)ws + align256(sizeof(float) * (size_t)B * m * plan->n_det);
-    auto mark = [&](int i) -> cudaError_t { return ev ? cudaEventRecord(ev[i], s) : cudaSuccess; };
+    // Under stream capture the stage events become external event-record nodes of the
+    // graph, so every replay records them (and their elapsed times stay meaningful).
+    unsigned ev_flags = cudaEventRecordDefault;
+    if (ev) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        SKEI_CUDA(cudaStreamIsCapturing(s, &cs));
+        if (cs == cudaStreamCaptureStatusActive) ev_flags = cudaEventRecordExternal;
+    }
+    auto mark = [&](int i) -> cudaError_t {
+        return ev ? cudaEventRecordWithFlags(ev[i], s, ev_flags) : cudaSuccess;
+    };
     const float fbp_scale = (float)(M_PI / (2.0 * m));
 
     SKEI_CUDA(mark(0));

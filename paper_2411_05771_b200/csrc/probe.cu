@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kProbeThreads) k_smem_probe(float *sink, int i
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
-            const float4 v = buf[(base + u * 128) & (kProbeBuf - 1)];
+            const float4 v = buf[(base + u * 64) & (kProbeBuf - 1)];  // 32 distinct slots
             acc.x += v.x;
             acc.y += v.y;
             acc.z += v.z;

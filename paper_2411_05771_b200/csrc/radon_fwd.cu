@@ -216,13 +216,19 @@ __global__ void __cluster_dims__(kS, 1, 1) __launch_bounds__(kThreads, 3)
                 tact[t] = __any_sync(0xffffffffu, act);
             }
         }
-#pragma unroll 1
-        for (int l = 0; l < nl; ++l) {
-            const float *srow = stage + (l * pitch + kPadL) * BB;
-            const float lf = (float)l;
+        // Two-level accumulation: the R lines of this block are summed into blk, which is
+        // then added to the running total (keeps fp32 rounding at ~1e-7 of the total).
 #pragma unroll
-            for (int t = 0; t < kMaxT; ++t) {
-                if (tact[t]) {
+        for (int t = 0; t < kMaxT; ++t) {
+            if (!tact[t]) continue;
+            float blk[BB];
+#pragma unroll
+            for (int b = 0; b < BB; ++b) blk[b] = 0.f;
+#pragma unroll 2
+            for (int l = 0; l < nl; ++l) {
+                const float *srow = stage + (l * pitch + kPadL) * BB;
+                const float lf = (float)l;
+                {
                     const float apos = fmaf(lf, tplf[t], tfrac[t]);
                     const float cf = floorf(apos - tsec[t]) + 1.f;
                     int ci = tbase[t] + (int)cf;
@@ -239,9 +245,11 @@ __global__ void __cluster_dims__(kS, 1, 1) __launch_bounds__(kThreads, 3)
                     ld_px<BB>(px + 2 * BB, v2);
 #pragma unroll
                     for (int b = 0; b < BB; ++b)
-                        acc[t][b] = fmaf(w2, v2[b], fmaf(w1, v1[b], fmaf(w0, v0[b], acc[t][b])));
+                        blk[b] = fmaf(w2, v2[b], fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b])));
                 }
             }
+#pragma unroll
+            for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
         }
         __syncthreads();
     }
