@@ -59,8 +59,9 @@ typedef void *skei_stream; /* cudaStream_t */
 /* Geometry of one CT system: n x n images, n_det detector bins, n_full angles on
  * [0, pi).  fft_len = ramp FFT length P: a power of two >= 2*n_det - 1 (the length
  * at which the zero-padded circular convolution equals the linear one, DESIGN.md
- * §5 "ramp"); 0 selects the smallest such power of two.  Limits: 2 <= n <= 4096,
- * 1 <= n_det <= 8192, 1 <= n_full <= 16384, P <= 16384. */
+ * §7 "k_ramp"); 0 selects the smallest such power of two.  Limits: 2 <= n <= 1792
+ * (a line block of the forward projector, (n + 8) x 128 bytes, must fit in one SM's
+ * shared memory), 1 <= n_det <= 3072, 1 <= n_full <= 16384, P <= 16384. */
 typedef struct {
     int32_t n;
     int32_t n_det;
@@ -82,8 +83,10 @@ skei_status skei_plan_geometry(const skei_plan *plan, skei_geometry *out); /* re
 const char *skei_status_string(skei_status status);     /* static string, never NULL */
 const char *skei_last_cuda_error(void);                  /* thread-local, after SKEI_ERR_CUDA */
 
-/* Device scratch needed by skei_fbp / skei_ei_residual / skei_pass for `batch`
- * images and sketch size m (bytes; 256-byte aligned pieces). */
+/* Device scratch needed by skei_radon_fwd / skei_fbp / skei_ei_residual / skei_pass
+ * for `batch` images and sketch size m (bytes; 256-byte aligned pieces): the filtered
+ * sinogram, the residual partial sums and four packed copies of the images (the forward
+ * projector's TMA-friendly input layout, ~4 * batch * n^2 floats). */
 size_t skei_workspace_bytes(const skei_plan *plan, int32_t batch, int32_t m);
 
 /* ---------------------------------------------------------------- a1: draws --
@@ -122,11 +125,12 @@ skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32
  * th = theta_{idx_b[k]} (BASELINE.json north_star projector; PAPER.md L283
  * "discrete radon transform"; sketched rows L92 A_S := S A).  Computed as a
  * gather per (angle, detector bin) — no atomics.  x: [B][n][n]; p: [B][m][n_det].
- * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL,
- * idx_stride not 0 or m). */
+ * The images are first packed into ws (line blocks), so ws must hold
+ * >= skei_workspace_bytes(plan, B, m) bytes.  Errors: SKEI_ERR_SHAPE (B < 1, m < 1
+ * or m > n_full), SKEI_ERR_ARG (NULL, idx_stride not 0 or m, ws too small). */
 skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int32_t B,
-                           const int32_t *idx, int32_t m, int32_t idx_stride,
-                           skei_stream stream);
+                           const int32_t *idx, int32_t m, int32_t idx_stride, void *ws,
+                           size_t ws_bytes, skei_stream stream);
 
 /* ---------------------------------------------------- a5/a8: adjoint A_S^T ------
  * x[b] = scale * A_S^T p[b]: the exact transpose of skei_radon_fwd (linear

@@ -76,7 +76,7 @@ def lib():
             "skei_draw": ([u64, u64, u64, i32, i32, i32, vp, vp], st),
             "skei_draw_device": ([u64, u64, u64, i32, i32, i32, i32, i32, vp, vp, vp], st),
             "skei_rotate": ([vp, vp, vp, i32, vp, i32, vp], st),
-            "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp], st),
+            "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
             "skei_radon_adj": ([vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, vp], st),
             "skei_ramp_filter": ([vp, vp, vp, i32, vp], st),
             "skei_fbp": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
@@ -214,11 +214,14 @@ def rotate(plan: Plan, x: torch.Tensor, g: torch.Tensor, out: torch.Tensor | Non
     return out
 
 
-def radon_fwd(plan: Plan, x: torch.Tensor, idx: torch.Tensor, out: torch.Tensor | None = None):
+def radon_fwd(plan: Plan, x: torch.Tensor, idx: torch.Tensor, out: torch.Tensor | None = None,
+              ws: torch.Tensor | None = None):
     B, m = x.shape[0], idx.shape[-1]
     p = torch.empty(B, m, plan.n_det, dtype=torch.float32, device=x.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
     _check(lib().skei_radon_fwd(plan.handle, _ptr(x, name="x"), _ptr(p, name="p"), B,
-                                _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m), _stream(x)),
+                                _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                _ptr(ws, torch.uint8, "ws"), ws.numel(), _stream(x)),
            "skei_radon_fwd")
     return p
 

@@ -51,6 +51,32 @@ double ramlak2(long n) {  // doubled Ram-Lak kernel h2 (R8)
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
+// Workspace: [q: B*m*n_det floats][residual partials][4 packed images: x1 rows/cols, x2
+// rows/cols, each pack_floats() for the largest image group]
+struct WsLayout {
+    size_t q, res, pack[4], total;
+};
+WsLayout ws_layout(const skei_plan *plan, int B, int m) {
+    WsLayout w;
+    size_t off = 0;
+    w.q = off;
+    off += align256(sizeof(float) * (size_t)B * m * plan->n_det);
+    w.res = off;
+    off += align256(residual_ws_bytes(plan, B, m));
+    size_t pk = 0;
+    for (int bb = 1; bb <= 4; bb *= 2) {
+        const size_t f = pack_floats(plan, B, bb);
+        if (f > pk) pk = f;
+    }
+    for (int i = 0; i < 4; ++i) {
+        w.pack[i] = off;
+        off += align256(sizeof(float) * pk);
+    }
+    w.total = off;
+    return w;
+}
+inline float *ws_f(void *ws, size_t off) { return reinterpret_cast<float *>((char *)ws + off); }
+
 skei_status check_idx_args(const skei_plan *plan, int B, const int32_t *idx, int m,
                            int idx_stride) {
     if (!plan || !idx) return SKEI_ERR_ARG;
@@ -83,7 +109,7 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     if (!geom || !out) return SKEI_ERR_ARG;
     *out = nullptr;
     const int n = geom->n, n_det = geom->n_det, n_full = geom->n_full;
-    if (n < 2 || n > 4096 || n_det < 1 || n_det > 8192 || n_full < 1 || n_full > 16384)
+    if (n < 2 || n > 1792 || n_det < 1 || n_det > 3072 || n_full < 1 || n_full > 16384)
         return SKEI_ERR_CONFIG;
     int P = geom->fft_len;
     if (P == 0) {
@@ -179,8 +205,7 @@ skei_status skei_plan_geometry(const skei_plan *plan, skei_geometry *out) {
 
 size_t skei_workspace_bytes(const skei_plan *plan, int32_t batch, int32_t m) {
     if (!plan || batch < 1 || m < 1) return 0;
-    size_t q = align256(sizeof(float) * (size_t)batch * m * plan->n_det);
-    return q + align256(residual_ws_bytes(plan, batch, m));
+    return ws_layout(plan, batch, m).total;
 }
 
 skei_status skei_draw(uint64_t seed, uint64_t iter, uint64_t image, int32_t n_full, int32_t m,
@@ -219,14 +244,19 @@ skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32
 }
 
 skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int32_t B,
-                           const int32_t *idx, int32_t m, int32_t idx_stride,
-                           skei_stream stream) {
+                           const int32_t *idx, int32_t m, int32_t idx_stride, void *ws,
+                           size_t ws_bytes, skei_stream stream) {
     skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
     if (st != SKEI_OK) return st;
-    if (!x || !p) return SKEI_ERR_ARG;
+    if (!x || !p || !ws) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
-    FwdJob job{x, p};
-    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, (cudaStream_t)stream));
+    const WsLayout w = ws_layout(plan, B, m);
+    cudaStream_t s = (cudaStream_t)stream;
+    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1])};
+    SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, pick_bb(B, idx_stride), s));
+    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), p};
+    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, s));
     return SKEI_OK;
 }
 
@@ -260,7 +290,7 @@ skei_status skei_fbp(const skei_plan *plan, const float *p, float *x, int32_t B,
     if (m_total < m) return SKEI_ERR_ARG;
     if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
-    float *q = (float *)ws;
+    float *q = ws_f(ws, ws_layout(plan, B, m).q);
     cudaStream_t s = (cudaStream_t)stream;
     SKEI_CUDA(launch_ramp(plan, p, q, B * m, s));
     AdjJob job{q, x, (float)(M_PI / (2.0 * (double)m_total))};
@@ -278,7 +308,7 @@ skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float
     if (!p1 || !y || !x2 || !x3 || !mc || !ei || !ws) return SKEI_ERR_ARG;
     if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
-    char *w = (char *)ws + align256(sizeof(float) * (size_t)B * m * plan->n_det);
+    void *w = ws_f(ws, ws_layout(plan, B, m).res);
     SKEI_CUDA(launch_residual(plan, p1, y, idx, m, idx_stride, x2, x3, B, mc, ei, r, w,
                               (cudaStream_t)stream));
     return SKEI_OK;
@@ -299,7 +329,8 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
     if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
-    char *wres = (char *)ws + align256(sizeof(float) * (size_t)B * m * plan->n_det);
+    const WsLayout wl = ws_layout(plan, B, m);
+    void *wres = ws_f(ws, wl.res);
     // Under stream capture the stage events become external event-record nodes of the
     // graph, so every replay records them (and their elapsed times stay meaningful).
     unsigned ev_flags = cudaEventRecordDefault;
@@ -314,11 +345,15 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     const float fbp_scale = (float)(M_PI / (2.0 * m));
 
     SKEI_CUDA(mark(0));
-    // a2: x2 = T_g x1
-    SKEI_CUDA(launch_rotate(plan, x1, o->x2, B, g_deg, g_stride, s));
+    // a2: x2 = T_g x1, fused with packing x1 and x2 for the forward projector
+    RotPackJob rj[2] = {
+        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1])},
+        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3])}};
+    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, pick_bb(B, idx_stride), s));
     SKEI_CUDA(mark(1));
     // a3: p1 = A_S x1 and p2 = A_S x2 in one launch
-    FwdJob fj[2] = {{x1, o->p1}, {o->x2, o->p2}};
+    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1},
+                    {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2}};
     SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, s));
     SKEI_CUDA(mark(2));
     // a4: q = ramp(p2)

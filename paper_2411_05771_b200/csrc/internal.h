@@ -38,17 +38,33 @@ inline Geom geom_of(const skei_plan *p) {
 }
 
 // ---- launchers (return cudaGetLastError()) ----
-// Up to two independent (input, output) pairs share one launch (e.g. A_S x1 and A_S x2).
-struct FwdJob { const float *x; float *p; };
+// Packed forward-projector input (rotate.cu): for image group g (BB images), class
+// (rows / cols) and block of R = 32/BB lines, [n pixels][R lines][BB images] floats.
+size_t pack_floats(const skei_plan *plan, int B, int bb);  // one packed copy (one class)
+struct RotPackJob {
+    const float *x;      // [B][n][n]
+    float *out;          // plain output [B][n][n] or NULL
+    const int32_t *g;    // rotation (device) or NULL = identity
+    int g_stride;        // 0 shared, 1 per image
+    float *xr, *xc;      // row- / col-packed outputs or NULL
+};
+struct RotPackArgs {
+    RotPackJob job[2];
+    int n, B, nblk, tiles_c;
+};
+cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
+                               int bb, cudaStream_t s);
+cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
+                          const int32_t *g, int g_stride, cudaStream_t s);
+
+// Forward projector on packed input; up to two jobs (e.g. A_S x1 and A_S x2) per launch.
+struct FwdJob { const float *xr, *xc; float *p; };
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s);
 
 struct AdjJob { const float *p; float *x; float scale; };
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s);
-
-cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
-                          const int32_t *g, int g_stride, cudaStream_t s);
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s);

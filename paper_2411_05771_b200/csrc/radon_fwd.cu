@@ -1,59 +1,117 @@
 // radon_fwd.cu — a3: p = A_S x, the pixel-driven projector with linear detector
 // interpolation, A[th, s] = sum_p x_p max(0, 1 - |x_p cos th + y_p sin th - s|/ds)
-// (BASELINE.json north_star), "organised as a per-(angle, detector-strip) gather so no
-// global atomics are needed".
+// (BASELINE.json north_star; R1-R4 in DESIGN.md), "organised as a per-(angle,
+// detector-strip) gather so no global atomics are needed".
 //
-// Design (DESIGN.md §5 "radon_fwd"):
-//   * Angles split into two classes by an exact integer test on the angle index:
-//     row class (|cos| >= |sin|: 4i <= n_full or 4i >= 3 n_full) marches over image rows,
-//     column class marches over image columns.  Along a line the pixel positions map to
-//     the detector with slope beta (|beta| >= 1/sqrt 2), so every (bin, line) pair has at
-//     most 3 candidate pixels: the first integer above a* - 1/|beta| and the next two,
-//     where a* is the line position that projects exactly onto the bin centre.
-//   * One CTA = (class, group of K angles of that class, batch group of BB images that
-//     share the angle list, quarter of the lines).  The four line-quarters of a work
-//     unit form a thread-block cluster: each CTA streams its quarter of the image through
-//     shared memory in blocks of R lines (cp.async), interleaved [line][pixel][image] so
-//     one LDS.128 fetches a candidate pixel of 4 images, and accumulates its partial
-//     projection in registers; at the end the partials are summed across the cluster
-//     through distributed shared memory in fixed rank order (deterministic, no atomics).
-//   * Work items: warp task = (angle, 32 consecutive bins); a warp owns up to 6 tasks,
-//     lane = bin.  Per (task, line): a* from an fp64 per-block base plus an fp32 local
-//     offset (split precision), 3 hat weights, 3 LDS.BB, 3*BB FFMA.
-//   * A task skips a line block when none of its 32 bins sees the block (warp vote).
+// Design (DESIGN.md §7 "k_radon_fwd"):
+//   * Angles are split by an exact integer test on the angle index into the row class
+//     (|cos| >= |sin|: 4i <= n_full or 4i >= 3 n_full; lines = image rows) and the column
+//     class (lines = image columns).  Along a line the pixel index maps to the detector
+//     with slope beta (|beta| >= 1/sqrt 2), so each (bin, line) pair has at most 3 candidate
+//     pixels: the first integer above a* - 1/|beta| and the next two, where a* is the line
+//     position that projects exactly onto the bin centre.
+//   * Input is the packed copy written by k_rotate_pack (rotate.cu): per image group and
+//     class, blocks of R = 32/BB lines stored [pixel][line][image] — 128 contiguous bytes
+//     per pixel — so a whole block is ONE TMA bulk copy (cp.async.bulk + mbarrier,
+//     double-buffered, issued by one thread: no staging instructions, no registers) and one
+//     LDS.BB fetches a candidate pixel of BB images.
+//   * Work unit = (job, group of BB images sharing the sketch, class, group of K angles);
+//     the S CTAs of a thread-block cluster (S chosen at launch to fill the waves) split the
+//     unit's lines.  Staged pixels are reused by all K angles of the unit.
+//   * Bank-conflict-free gathers: lane L processes the lines of a block in the skewed
+//     order l = (L + s) mod R.  The lanes of one shared-memory phase (8 lanes for LDS.128,
+//     16 for LDS.64, 32 for LDS.32) then read R distinct line slots, i.e. distinct banks,
+//     whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way conflicts at
+//     every angle with |beta| < 1 because 8 bins span more than 8 pixels).
+//   * 1024 threads (64 registers each), one CTA per SM.  Task = (angle, 32 consecutive
+//     bins), lane = bin; the K x chunks tasks are dealt round-robin to the 32 warps (each
+//     warp gets a mix of angles, whose footprints differ); a thread owns up to kMaxT tasks
+//     and keeps BB accumulators per task in registers: K = 32 kMaxT / chunks angles.
+//   * Decoupled pipeline: no per-block barrier.  The last warp to finish a staged block
+//     (shared-memory counter) refills its buffer with the block nbuf ahead, so warps drift
+//     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
+//   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset < R (split
+//     precision), 3 hat weights, 3 LDS.BB (the third skipped when its weight
+//     is 0), 3*BB FFMA.  The R lines of a block are summed into a partial before it is
+//     added to the running total (two-level summation).  A chunk skips a block none of its
+//     32 bins sees.
+//   * End: per-CTA partial projections -> shared memory -> fixed-rank-order sum across the
+//     cluster through distributed shared memory (deterministic, no atomics) -> p.
 #include <cooperative_groups.h>
 
 #include "internal.h"
 
-namespace cg = cooperative_groups;
-
 namespace skei {
 namespace {
 
-constexpr int kThreads = 256;
+namespace cg = cooperative_groups;
+
+constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxT = 6;     // tasks per warp
-constexpr int kS = 4;        // line split = cluster size
-constexpr int kKMax = 16;    // angles per CTA
-constexpr int kPadL = 4;     // zero pixels left of each staged line (right pad >= 5)
+constexpr int kMaxT = 6;    // 32-bin chunks per thread (registers left for load pipelining)
+constexpr int kKMax = 32;   // angles per CTA
+constexpr int kPadL = 4;    // zero pixel columns left of the line data
+constexpr int kPadR = 4;    // ... and right of it (candidates reach n + 2)
+constexpr int kColF = 32;   // floats per staged pixel column (R * BB)
 
 struct FwdArgs {
     FwdJob job[2];
     const int32_t *idx;
     int m, idx_stride, B;
-    int K;       // angles per CTA
+    int K;       // angles per CTA: K * chunks <= kWarps * kMaxT tasks
     int chunks;  // ceil(n_det / 32)
-    int pitch;   // staged pixels per line (>= n + 9, = 1 mod 8 for conflict-free staging)
+    int nblk;    // packed blocks per image group (ceil(n / R))
+    int nbuf;    // staging buffers (2 = double-buffered)
     Geom g;
 };
 
-__device__ inline void cp_async4(float *smem, const float *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+// ---- TMA bulk copy + mbarrier (sm_90+ async proxy), inline PTX
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
 }
-__device__ inline void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::);
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until the phase
+    // completes (or the hint expires) instead of spinning on issue slots other warps need
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
+// One packed block (n pixel columns of 128 B) -> the interior of a staging buffer.
+__device__ __forceinline__ void issue_block(float *buf, const float *src, int n, uint64_t *bar) {
+    const unsigned bytes = (unsigned)n * 128u;
+    mbar_expect_tx(bar, bytes);
+    constexpr unsigned kPiece = 32768u;
+    for (unsigned off = 0; off < bytes; off += kPiece) {
+        const unsigned len = bytes - off < kPiece ? bytes - off : kPiece;
+        bulk_g2s(reinterpret_cast<char *>(buf) + off, reinterpret_cast<const char *>(src) + off, len, bar);
+    }
 }
 
 template <int BB>
@@ -63,7 +121,7 @@ template <> struct Px<2> { using T = float2; };
 template <> struct Px<4> { using T = float4; };
 
 template <int BB>
-__device__ inline void ld_px(const float *p, float (&v)[BB]) {
+__device__ __forceinline__ void ld_px(const float *p, float (&v)[BB]) {
     const typename Px<BB>::T t = *reinterpret_cast<const typename Px<BB>::T *>(p);
     const float *pt = reinterpret_cast<const float *>(&t);
 #pragma unroll
@@ -71,26 +129,27 @@ __device__ inline void ld_px(const float *p, float (&v)[BB]) {
 }
 
 template <int BB>
-__global__ void __cluster_dims__(kS, 1, 1) __launch_bounds__(kThreads, 3)
-    k_radon_fwd(FwdArgs a) {
-    constexpr int R = 32 / BB;  // lines per staged block (R * BB = 32 floats per pixel column)
-    extern __shared__ __align__(16) float stage[];  // [R][pitch][BB]; partials at the end
+__global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
+    constexpr int R = kColF / BB;
+    extern __shared__ __align__(128) float smem[];  // nbuf x [n + pads][R][BB]; partials at end
+    __shared__ __align__(8) uint64_t full[3];
+    __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
     __shared__ float sAbsB[kKMax], sSec[kKMax], sPlf[kKMax];
     __shared__ int sSlot[kKMax];
     __shared__ int sCount;
 
     cg::cluster_group cluster = cg::this_cluster();
+    const int S = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
-    const int unit = blockIdx.x / kS;
+    const int unit = blockIdx.x / S;
     const int cls = unit & 1, grp = unit >> 1;
     const FwdJob job = blockIdx.z ? a.job[1] : a.job[0];
     const int b0 = blockIdx.y * BB;
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
     const int n = a.g.n, n_det = a.g.n_det, n_full = a.g.n_full;
-    const int pitch = a.pitch;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int K = a.K;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     // ---- 1. the grp-th group of K angles of class cls, in sketch-slot order
     if (threadIdx.x < 32) {
@@ -137,144 +196,142 @@ __global__ void __cluster_dims__(kS, 1, 1) __launch_bounds__(kThreads, 3)
         sSec[threadIdx.x] = (float)(1.0 / ab);
         sPlf[threadIdx.x] = (float)Pl;
     }
-    // zero pads: positions [0, kPadL) and [kPadL + n, pitch) of every staged line
-    for (int e = threadIdx.x; e < R * (pitch - n) * BB; e += kThreads) {
-        const int b = e % BB;
-        const int q = (e / BB) % (pitch - n);
-        const int l = e / (BB * (pitch - n));
-        const int pos = q < kPadL ? q : n + q;
-        stage[(l * pitch + pos) * BB + b] = 0.f;
+    // zero pad columns of every buffer (never written by the bulk copies)
+    const int stage_f = (n + kPadL + kPadR) * kColF;
+    for (int e = threadIdx.x; e < a.nbuf * (kPadL + kPadR) * kColF; e += kThreads) {
+        const int bi = e / ((kPadL + kPadR) * kColF);
+        const int e2 = e - bi * (kPadL + kPadR) * kColF;
+        const int q = e2 / kColF, w = e2 - q * kColF;
+        const int col = q < kPadL ? q : kPadL + n + (q - kPadL);
+        smem[bi * stage_f + col * kColF + w] = 0.f;
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&full[2], 1);
+        done[0] = done[1] = done[2] = 0;
+        fence_mbar_init();
     }
     __syncthreads();
 
-    // ---- 3. tasks of this thread
-    int tk[kMaxT], tj[kMaxT];
-    bool tvalid[kMaxT];
-    float tab[kMaxT], tsec[kMaxT], tplf[kMaxT];
-    float acc[kMaxT][BB];
-#pragma unroll
-    for (int t = 0; t < kMaxT; ++t) {
-        const int task = warp + kWarps * t;
-        tk[t] = task / a.chunks;
-        tj[t] = (task % a.chunks) * 32 + lane;
-        tvalid[t] = tk[t] < kcnt;
-        const int kk = tvalid[t] ? tk[t] : 0;
-        tab[t] = sAbsB[kk];
-        tsec[t] = sSec[kk];
-        tplf[t] = sPlf[kk];
-#pragma unroll
-        for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
+    // this CTA's lines: whole packed blocks
+    const int blocks_per = (a.nblk + S - 1) / S;
+    const int blk0 = min(a.nblk, rank * blocks_per), blk1 = min(a.nblk, blk0 + blocks_per);
+    const int nb = blk1 - blk0;
+    const float *xsrc = (cls ? job.xc : job.xr) + (long)blockIdx.y * a.nblk * n * kColF;
+    // TMA pipeline: block q lives in buffer q % nbuf.  Blocks 0..nbuf-1 are issued up front;
+    // block q + nbuf is issued by the last warp to finish block q (shared counter), so warps
+    // are never barrier-synchronised per block and can drift up to nbuf - 1 blocks apart.
+    const int nbuf = a.nbuf;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < min(nbuf, nb); ++q)
+            issue_block(smem + q * stage_f + kPadL * kColF, xsrc + (long)(blk0 + q) * n * kColF, n,
+                        &full[q]);
     }
 
-    const int lines_per = (n + kS - 1) / kS;
-    const int L0 = rank * lines_per, L1 = min(n, L0 + lines_per);
-    const long nn = (long)n * n;
-    const float *xb = job.x + (long)b0 * nn;
+    // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps, so every
+    // warp holds a mix of angles (near-0 and near-45 degree angles have different footprints)
+    const int ntask = kcnt * a.chunks;
+    const float fn1 = (float)(n - 1);
+    float acc[kMaxT][BB];
+#pragma unroll
+    for (int t = 0; t < kMaxT; ++t)
+#pragma unroll
+        for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
 
-    for (int lb = L0; lb < L1; lb += R) {
-        const int nl = min(R, L1 - lb);
-        // ---- stage R lines (source lines clamped into the image; extra lines unused)
-        if (cls == 0) {
-#pragma unroll 1
-            for (int l = 0; l < R; ++l) {
-                const int row = min(lb + l, n - 1);
-                for (int e = threadIdx.x; e < n * BB; e += kThreads) {
-                    const int b = e % BB, c = e / BB;
-                    cp_async4(stage + (l * pitch + kPadL + c) * BB + b,
-                              xb + (long)b * nn + (long)row * n + c);
-                }
-            }
-        } else {
-            for (int e = threadIdx.x; e < n * R * BB; e += kThreads) {
-                const int b = e % BB, l = (e / BB) % R, r = e / (BB * R);
-                const int col = min(lb + l, n - 1);
-                cp_async4(stage + (l * pitch + kPadL + r) * BB + b,
-                          xb + (long)b * nn + (long)r * n + col);
-            }
-        }
-        cp_async_wait_all();
-        __syncthreads();
-
-        // ---- per-task base of this block (fp64) and warp-level activity
-        int tbase[kMaxT];
-        float tfrac[kMaxT];
-        bool tact[kMaxT];
+    for (int i = 0; i < nb; ++i) {
+        const int lb = (blk0 + i) * R;
+        const int cb = i % nbuf;
+        const float *cur = smem + cb * stage_f;
+        mbar_wait(&full[cb], (unsigned)((i / nbuf) & 1));
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t) {
-            tbase[t] = 0;
-            tfrac[t] = 0.f;
-            tact[t] = false;
-            if (tvalid[t]) {  // warp-uniform
-                const int k = tk[t];
-                const double ad = sP0[k] + (double)tj[t] * sPj[k] + (double)lb * sPl[k];
-                const double fl = floor(ad);
-                tbase[t] = (int)fl;
-                tfrac[t] = (float)(ad - fl);
-                const double ae = ad + (double)(nl - 1) * sPl[k];
-                const double lo = fmin(ad, ae), hi = fmax(ad, ae);
-                const bool act = tj[t] < n_det && hi + tsec[t] > 0.0 && lo - tsec[t] < n - 1.0;
-                tact[t] = __any_sync(0xffffffffu, act);
-            }
-        }
-        // Two-level accumulation: the R lines of this block are summed into blk, which is
-        // then added to the running total (keeps fp32 rounding at ~1e-7 of the total).
-#pragma unroll
-        for (int t = 0; t < kMaxT; ++t) {
-            if (!tact[t]) continue;
+            const int tau = warp + kWarps * t;
+            if (tau >= ntask) break;  // warp-uniform
+            const int k = tau / a.chunks;
+            const int chunk = tau - k * a.chunks;
+            const int j = chunk * 32 + lane;
+            const double Pl = sPl[k];
+            const double ad = sP0[k] + (double)lb * Pl + (double)j * sPj[k];
+            const double fl = floor(ad);
+            const int base = (int)fl;
+            const float frac = (float)(ad - fl);
+            const float ab = sAbsB[k], sec = sSec[k], plf = sPlf[k];
+            // does any bin of this chunk see a line of this block?
+            const float span = (float)(R - 1) * plf;
+            const float lo = (float)base + frac + fminf(0.f, span);
+            const float hi = (float)base + frac + fmaxf(0.f, span);
+            const bool act = j < n_det && hi + sec > 0.f && lo - sec < fn1;
+            if (!__any_sync(0xffffffffu, act)) continue;
+            const float c1 = 2.f * ab - 1.f, c2 = 2.f - 3.f * ab;
+            const float fs = frac - sec;
             float blk[BB];
 #pragma unroll
             for (int b = 0; b < BB; ++b) blk[b] = 0.f;
-#pragma unroll 2
-            for (int l = 0; l < nl; ++l) {
-                const float *srow = stage + (l * pitch + kPadL) * BB;
-                const float lf = (float)l;
-                {
-                    const float apos = fmaf(lf, tplf[t], tfrac[t]);
-                    const float cf = floorf(apos - tsec[t]) + 1.f;
-                    int ci = tbase[t] + (int)cf;
-                    ci = min(max(ci, -3), n);
-                    const float d0 = (cf - apos) * tab[t];
-                    const float d1 = d0 + tab[t], d2 = d1 + tab[t];
-                    const float w0 = fmaxf(0.f, 1.f - fabsf(d0));
-                    const float w1 = fmaxf(0.f, 1.f - fabsf(d1));
-                    const float w2 = fmaxf(0.f, 1.f - fabsf(d2));
-                    const float *px = srow + ci * BB;
-                    float v0[BB], v1[BB], v2[BB];
-                    ld_px<BB>(px, v0);
-                    ld_px<BB>(px + BB, v1);
-                    ld_px<BB>(px + 2 * BB, v2);
 #pragma unroll
-                    for (int b = 0; b < BB; ++b)
-                        blk[b] = fmaf(w2, v2[b], fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b])));
+            for (int s = 0; s < R; ++s) {
+                const int l = (lane + s) & (R - 1);
+                // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
+                // phi = e - floor(e) the hat weights of the 3 candidates are
+                //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
+                const float e = fmaf((float)l, plf, fs);
+                const float fl2 = floorf(e);
+                const float phi = e - fl2;
+                int ci = base + (int)fl2 + 1;
+                ci = min(max(ci, -3), n);
+                const float w0 = fmaf(-ab, phi, ab);
+                const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
+                const float w2 = fmaf(ab, phi, c2);
+                const float *px = cur + (ci + kPadL) * kColF + l * BB;
+                float v0[BB], v1[BB], v2[BB];
+                ld_px<BB>(px, v0);
+                ld_px<BB>(px + kColF, v1);
+#pragma unroll
+                for (int b = 0; b < BB; ++b) blk[b] = fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b]));
+                if (w2 > 0.f) {
+                    ld_px<BB>(px + 2 * kColF, v2);
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) blk[b] = fmaf(w2, v2[b], blk[b]);
                 }
             }
 #pragma unroll
             for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
         }
-        __syncthreads();
+        // release the buffer; the last warp out refills it with block i + nbuf
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();  // this warp's reads of the buffer are complete
+            const int old = atomicAdd(&done[cb], 1);
+            if (old == kWarps * (i / nbuf + 1) - 1 && i + nbuf < nb) {
+                fence_proxy_async();  // generic-proxy reads -> async-proxy writes
+                issue_block(smem + cb * stage_f + kPadL * kColF,
+                            xsrc + (long)(blk0 + i + nbuf) * n * kColF, n, &full[cb]);
+            }
+        }
     }
+    __syncthreads();  // all blocks consumed: the buffers become the partials array
 
-    // ---- 4. partials -> shared memory, then fixed-order sum across the cluster (DSMEM)
-    float *part = stage;  // [kcnt][n_det][BB]
+    // ---- 4. partials -> shared memory [kcnt][n_det][BB], then fixed-order cluster sum
+    float *part = smem;
 #pragma unroll
     for (int t = 0; t < kMaxT; ++t) {
-        if (tvalid[t] && tj[t] < n_det) {
+        const int tau = warp + kWarps * t;
+        if (tau >= ntask) break;
+        const int k = tau / a.chunks;
+        const int j = (tau - k * a.chunks) * 32 + lane;
+        if (j < n_det) {
 #pragma unroll
-            for (int b = 0; b < BB; ++b) part[((long)tk[t] * n_det + tj[t]) * BB + b] = acc[t][b];
+            for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
         }
     }
     cluster.sync();
     const int T = kcnt * n_det * BB;
-    const int per = (T + kS - 1) / kS;
+    const int per = (T + S - 1) / S;
     const int o0 = rank * per, o1 = min(T, o0 + per);
-    const float *rp[kS];
-#pragma unroll
-    for (int q = 0; q < kS; ++q) rp[q] = cluster.map_shared_rank(part, q);
     const long img_stride = (long)a.m * n_det;
     for (int o = o0 + threadIdx.x; o < o1; o += kThreads) {
         float s = 0.f;
-#pragma unroll
-        for (int q = 0; q < kS; ++q) s += rp[q][o];
+        for (int q = 0; q < S; ++q) s += cluster.map_shared_rank(part, q)[o];
         const int b = o % BB;
         const int kj = o / BB;
         const int k = kj / n_det, j = kj - k * n_det;
@@ -283,18 +340,55 @@ __global__ void __cluster_dims__(kS, 1, 1) __launch_bounds__(kThreads, 3)
     cluster.sync();
 }
 
+// Cluster size S (line split): the number of busy units is about jobs * groups * (m/K + 1);
+// pick S in [2, 8] so that busy CTAs fill whole waves of 2 CTAs per SM.
+int pick_cluster(long units, int num_sms, int ctas_per_sm) {
+    const long slots = (long)num_sms * ctas_per_sm;
+    int best = 4;
+    double best_cost = 1e30;
+    for (int S = 2; S <= 8; ++S) {
+        const long ctas = units * S;
+        const double waves = (double)((ctas + slots - 1) / slots);
+        const double cost = waves / S * (1.0 + 0.02 * S);  // per-CTA reduction overhead
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = S;
+        }
+    }
+    return best;
+}
+
 template <int BB>
-cudaError_t launch_bb(const FwdArgs &a, int njobs, cudaStream_t s) {
-    constexpr int R = 32 / BB;
-    const size_t stage_f = (size_t)R * a.pitch * BB;
-    const size_t part_f = (size_t)a.K * a.g.n_det * BB;
-    const size_t smem = sizeof(float) * (stage_f > part_f ? stage_f : part_f);
+cudaError_t launch_bb(FwdArgs a, int njobs, int num_sms, cudaStream_t s) {
+    constexpr int R = kColF / BB;
+    a.nblk = (a.g.n + R - 1) / R;
+    const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
+    const size_t part_b = sizeof(float) * (size_t)a.K * a.g.n_det * BB;
+    const size_t limit = 225 * 1024;  // dynamic shared memory budget per CTA (1 CTA / SM)
+    a.nbuf = 3 * stage_b <= limit ? 3 : (2 * stage_b <= limit ? 2 : 1);
+    size_t smem = a.nbuf * stage_b;
+    if (part_b > smem) smem = part_b;
+    if (smem > limit) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (a.m + a.K - 1) / a.K;  // per class, worst case
-    dim3 grid((unsigned)(kS * 2 * ngroups), (unsigned)(a.B / BB), (unsigned)njobs);
-    k_radon_fwd<BB><<<grid, kThreads, smem, s>>>(a);
+    const long busy = (long)njobs * (a.B / BB) * ((a.m + a.K - 1) / a.K + 1);
+    const int S = pick_cluster(busy, num_sms, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(S * 2 * ngroups), (unsigned)(a.B / BB), (unsigned)njobs);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_radon_fwd<BB>, a);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -312,16 +406,13 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.g = geom_of(plan);
     a.chunks = (plan->n_det + 31) / 32;
     a.K = (kWarps * kMaxT) / a.chunks;
-    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > 48*32 bins not supported
     if (a.K > kKMax) a.K = kKMax;
-    int pitch = plan->n + 9;
-    while (pitch % 8 != 1) ++pitch;
-    a.pitch = pitch;
+    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * 32
     const int bb = pick_bb(B, idx_stride);
     switch (bb) {
-        case 4: return launch_bb<4>(a, njobs, s);
-        case 2: return launch_bb<2>(a, njobs, s);
-        default: return launch_bb<1>(a, njobs, s);
+        case 4: return launch_bb<4>(a, njobs, plan->num_sms, s);
+        case 2: return launch_bb<2>(a, njobs, plan->num_sms, s);
+        default: return launch_bb<1>(a, njobs, plan->num_sms, s);
     }
 }
 

@@ -41,7 +41,7 @@ def test_status_strings():
 def test_host_validation_without_device():
     L = sk.lib()
     # NULL plan / NULL pointers -> SKEI_ERR_ARG, nothing launched
-    assert L.skei_radon_fwd(None, None, None, 1, None, 1, 0, None) == 3
+    assert L.skei_radon_fwd(None, None, None, 1, None, 1, 0, None, 0, None) == 3
     assert L.skei_ramp_filter(None, None, None, 1, None) == 3
     assert L.skei_plan_create(None, 0, None) == 3
     g = sk._Geom(64, 91, 32, 100)  # fft_len not a power of two -> config error
