@@ -54,7 +54,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // Workspace: [q: B*m*n_det floats][residual partials][4 packed images: x1 rows/cols, x2
 // rows/cols, each pack_floats() for the largest image group]
 struct WsLayout {
-    size_t q, res, pack[4], total;
+    size_t q, res, pack[4], ctr, mcpart, eipart, fscr, total;
 };
 WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     WsLayout w;
@@ -72,6 +72,14 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
         w.pack[i] = off;
         off += align256(sizeof(float) * pk);
     }
+    w.ctr = off;  // 2 completion counters of the fused reductions
+    off += 256;
+    w.mcpart = off;
+    off += align256(sizeof(float) * (size_t)B * fwd_mc_slots(plan, B, m, 0));
+    w.eipart = off;
+    off += align256(sizeof(float) * adj_ei_part_floats(plan, B));
+    w.fscr = off;  // forward per-CTA partials
+    off += align256(sizeof(float) * fwd_scratch_floats(plan));
     w.total = off;
     return w;
 }
@@ -153,6 +161,14 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
         }
         for (int k = 0; k < P; ++k) ramp[k] = (float)(R[k <= P / 2 ? k : P - k] / (double)P);
     }
+    std::vector<double2> rot(360);  // (cos g, sin g), g in degrees; exact at multiples of 90
+    for (int g = 0; g < 360; ++g) {
+        if (g == 0) rot[g] = make_double2(1.0, 0.0);
+        else if (g == 90) rot[g] = make_double2(0.0, 1.0);
+        else if (g == 180) rot[g] = make_double2(-1.0, 0.0);
+        else if (g == 270) rot[g] = make_double2(0.0, -1.0);
+        else rot[g] = make_double2(std::cos(M_PI * g / 180.0), std::sin(M_PI * g / 180.0));
+    }
     std::vector<float2> tw(P / 2);
     for (int k = 0; k < P / 2; ++k) {
         double a = 2.0 * M_PI * (double)k / (double)P;
@@ -171,6 +187,9 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * n_full);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_ramp, sizeof(float) * P);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_tw, sizeof(float2) * (P / 2));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_rot, sizeof(double2) * 360);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_rot, rot.data(), sizeof(double2) * 360, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_trig, trig.data(), sizeof(double2) * n_full, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
@@ -191,6 +210,7 @@ void skei_plan_destroy(skei_plan *plan) {
     if (plan->d_trig) cudaFree(plan->d_trig);
     if (plan->d_ramp) cudaFree(plan->d_ramp);
     if (plan->d_tw) cudaFree(plan->d_tw);
+    if (plan->d_rot) cudaFree(plan->d_rot);
     delete plan;
 }
 
@@ -253,10 +273,12 @@ skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int3
     DeviceGuard guard(plan->device);
     const WsLayout w = ws_layout(plan, B, m);
     cudaStream_t s = (cudaStream_t)stream;
-    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1])};
-    SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, pick_bb(B, idx_stride), s));
-    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), p};
-    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, s));
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
+    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+    SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
+    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), p, nullptr, nullptr};
+    const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
+    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, scr, s));
     return SKEI_OK;
 }
 
@@ -345,31 +367,35 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     const float fbp_scale = (float)(M_PI / (2.0 * m));
 
     SKEI_CUDA(mark(0));
-    // a2: x2 = T_g x1, fused with packing x1 and x2 for the forward projector
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
+    // a2: x2 = T_g x1, fused with packing x1 and x2 for the forward projector (and zeroing
+    // the completion counters of the fused reductions below)
     RotPackJob rj[2] = {
-        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1])},
-        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3])}};
-    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, pick_bb(B, idx_stride), s));
+        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), ctr},
+        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), nullptr}};
+    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s));
     SKEI_CUDA(mark(1));
-    // a3: p1 = A_S x1 and p2 = A_S x2 in one launch
-    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1},
-                    {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2}};
-    SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, s));
+    // a3 + a7 (MC part): p1 = A_S x1 with r = p1 - y_S and mc = ||r||^2 fused into its
+    // epilogue, and p2 = A_S x2, in one launch
+    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1, y, o->r},
+                    {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
+    FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
+    const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
+    SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr));
     SKEI_CUDA(mark(2));
     // a4: q = ramp(p2)
     SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s));
     SKEI_CUDA(mark(3));
-    // a7 (MC part): r = p1 - y_S, mc
-    SKEI_CUDA(launch_residual(plan, o->p1, y, idx, m, idx_stride, nullptr, nullptr, B, o->mc,
-                              nullptr, o->r, wres, s));
-    SKEI_CUDA(mark(4));
-    // a5 + a8: xfbp = (pi/2m) A_S^T q and grad = 2 A_S^T r in one launch
+    SKEI_CUDA(mark(4));  // (the MC residual ran inside the forward launch)
+    // a5 + a8 (+ a7 EI part when x3 is the identity network's x_fbp): x_fbp = (pi/2m) A_S^T q
+    // and grad = 2 A_S^T r in one launch, ei = ||x2 - x_fbp||^2 fused into its epilogue
     AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale}, {o->r, o->grad, 2.0f}};
-    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s));
+    AdjEi eif{o->x2, ws_f(ws, wl.eipart), ctr + 1, o->ei};
+    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, x3_in ? nullptr : &eif));
     SKEI_CUDA(mark(5));
-    // a7 (EI part): ei = ||x2 - x3||^2, x3 = x3_in or the identity network's xfbp
-    SKEI_CUDA(launch_residual(plan, nullptr, nullptr, idx, m, idx_stride, o->x2,
-                              x3_in ? x3_in : o->xfbp, B, nullptr, o->ei, nullptr, wres, s));
+    if (x3_in)  // a7 (EI part) against a caller-provided x3
+        SKEI_CUDA(launch_residual(plan, nullptr, nullptr, idx, m, idx_stride, o->x2, x3_in, B,
+                                  nullptr, o->ei, nullptr, wres, s));
     SKEI_CUDA(mark(6));
     return SKEI_OK;
 }

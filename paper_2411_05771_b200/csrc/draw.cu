@@ -45,60 +45,58 @@ __host__ __device__ inline int draw_rotation(uint64_t seed, uint64_t iter, uint6
     return 1 + (int)mulhi_below(sm64_out(sm64_key(seed, kStreamRot, iter, image), 0), 360u);
 }
 
-// One block per drawn image: thread 0 runs the partial Fisher-Yates swaps in shared
-// memory, then the block compacts the chosen flags with a prefix scan, which emits the
-// subset already sorted ascending.
-__global__ void k_draw(uint64_t seed, uint64_t iter, uint64_t image0, int shared, int n_full,
-                       int m, int mode, int32_t *g_out, int32_t *idx_out) {
+// One warp per drawn image (32-thread blocks).  The lanes compute the Fisher-Yates targets
+// j_i = i + U(n_full - i) in parallel (each is a pure function of the word index), lane 0
+// applies the m swaps in shared memory in order, and the chosen set is compacted with
+// ballots, which emits it already sorted ascending (the same set as the host's sort).
+__global__ void __launch_bounds__(32) k_draw(uint64_t seed, uint64_t iter, uint64_t image0,
+                                             int shared, int n_full, int m, int mode,
+                                             int32_t *g_out, int32_t *idx_out) {
     extern __shared__ int sm[];
-    int *perm = sm;              // [n_full]
-    int *flag = sm + n_full;     // [n_full]
-    __shared__ int warp_tot[32];
+    int *perm = sm;           // [n_full]
+    int *tgt = sm + n_full;   // [m]
+    const int lane = threadIdx.x;
     const int b = blockIdx.x;
     const uint64_t image = shared ? ~0ULL : image0 + (uint64_t)b;
     int32_t *idx = idx_out + (size_t)b * m;
-    if (threadIdx.x == 0) g_out[b] = draw_rotation(seed, iter, image);
+    if (lane == 0) g_out[b] = draw_rotation(seed, iter, image);
     const uint64_t ksk = sm64_key(seed, kStreamSketch, iter, image);
     if (mode == 0) {
         const int nb = n_full / m;
         const int base = (int)mulhi_below(sm64_out(ksk, 0), (uint32_t)nb);
-        for (int k = threadIdx.x; k < m; k += blockDim.x) idx[k] = base + k * nb;
+        for (int k = lane; k < m; k += 32) idx[k] = base + k * nb;
         return;
     }
-    for (int i = threadIdx.x; i < n_full; i += blockDim.x) {
-        perm[i] = i;
-        flag[i] = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    for (int i = lane; i < n_full; i += 32) perm[i] = i;
+    for (int i = lane; i < m; i += 32)
+        tgt[i] = i + (int)mulhi_below(sm64_out(ksk, (uint64_t)i), (uint32_t)(n_full - i));
+    __syncwarp();
+    if (lane == 0) {
         for (int i = 0; i < m; ++i) {
-            int j = i + (int)mulhi_below(sm64_out(ksk, (uint64_t)i), (uint32_t)(n_full - i));
-            int t = perm[i];
+            const int j = tgt[i];
+            const int t = perm[i];
             perm[i] = perm[j];
             perm[j] = t;
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) flag[perm[i]] = 1;
-    __syncthreads();
-    // block-wide exclusive scan over flags, chunked by blockDim
+    __syncwarp();
+    // collect the m chosen values, then mark them in a flag array (perm is reused)
+    for (int i = lane; i < m; i += 32) {
+        const int v = perm[i];
+        tgt[i] = v;  // the chosen values (unsorted)
+    }
+    __syncwarp();
+    for (int i = lane; i < n_full; i += 32) perm[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) perm[tgt[i]] = 1;
+    __syncwarp();
     int carry = 0;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int base = 0; base < n_full; base += blockDim.x) {
-        int i = base + threadIdx.x;
-        int f = (i < n_full) ? flag[i] : 0;
-        unsigned bal = __ballot_sync(0xffffffffu, f);
-        int pre = __popc(bal & ((1u << lane) - 1u));
-        if (lane == 0) warp_tot[wid] = __popc(bal);
-        __syncthreads();
-        int woff = 0, tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            if (w < wid) woff += warp_tot[w];
-            tot += warp_tot[w];
-        }
-        if (f) idx[carry + woff + pre] = i;
-        carry += tot;
-        __syncthreads();
+    for (int base = 0; base < n_full; base += 32) {
+        const int i = base + lane;
+        const int f = (i < n_full) ? perm[i] : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (f) idx[carry + __popc(bal & ((1u << lane) - 1u))] = i;
+        carry += __popc(bal);
     }
 }
 
@@ -127,13 +125,13 @@ int host_draw(uint64_t seed, uint64_t iter, uint64_t image, int n_full, int m, i
 
 cudaError_t launch_draw(uint64_t seed, uint64_t iter, uint64_t image0, int count, int shared,
                         int n_full, int m, int mode, int32_t *g, int32_t *idx, cudaStream_t s) {
-    const size_t smem = (mode == 1) ? sizeof(int) * 2 * (size_t)n_full : 0;
+    const size_t smem = (mode == 1) ? sizeof(int) * ((size_t)n_full + m) : 0;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_draw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k_draw<<<count, 256, smem, s>>>(seed, iter, image0, shared, n_full, m, mode, g, idx);
+    k_draw<<<count, 32, smem, s>>>(seed, iter, image0, shared, n_full, m, mode, g, idx);
     return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@ struct skei_plan {
     double2 *d_trig;  // [n_full] (cos, sin) of theta_i = i*pi/n_full, fp64
     float *d_ramp;    // [fft_len] R[k] / P, fp32 (from an fp64 DFT)
     float2 *d_tw;     // [fft_len/2] exp(-2 pi i k / P), fp32 (from fp64)
+    double2 *d_rot;   // [360] (cos g, sin g) of g degrees, fp64, exact at multiples of 90
 };
 
 namespace skei {
@@ -47,9 +48,11 @@ struct RotPackJob {
     const int32_t *g;    // rotation (device) or NULL = identity
     int g_stride;        // 0 shared, 1 per image
     float *xr, *xc;      // row- / col-packed outputs or NULL
+    unsigned *zero;      // if set, block (0,0,0) zeroes zero[0..2] (pass counters)
 };
 struct RotPackArgs {
     RotPackJob job[2];
+    const double2 *rot;  // plan->d_rot
     int n, B, nblk, tiles_c;
 };
 cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
@@ -58,13 +61,42 @@ cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int
                           const int32_t *g, int g_stride, cudaStream_t s);
 
 // Forward projector on packed input; up to two jobs (e.g. A_S x1 and A_S x2) per launch.
-struct FwdJob { const float *xr, *xc; float *p; };
+// Job 0 may fuse the MC residual: y != NULL -> r = p - y_S (if r != NULL) and mc = sum r^2.
+struct FwdJob {
+    const float *xr, *xc;
+    float *p;
+    const float *y;  // full sinogram [B][n_full][n_det] or NULL (job 0 only)
+    float *r;        // residual [B][m][n_det] or NULL
+};
+struct FwdMc {
+    float *part;    // [B][fwd_mc_slots] partial sums
+    unsigned *ctr;  // completion counter, zero before the launch (self-resetting)
+    float *out;     // mc [B]
+};
+// Forward scratch: work-queue counter (zero before the launch) and per-CTA partials.
+struct FwdScratch {
+    unsigned *queue;
+    float *part;  // fwd_scratch_floats
+};
+size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride);
+size_t fwd_scratch_floats(const skei_plan *plan);
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
-                             const int32_t *idx, int m, int idx_stride, cudaStream_t s);
+                             const int32_t *idx, int m, int idx_stride, const FwdScratch &scr,
+                             cudaStream_t s, const FwdMc *mc = nullptr);
 
+// Backprojection; up to two jobs sharing one angle list (FBP of q and gradient of r).
+// Job 0 may fuse ei = sum (x2 - x_job0)^2 (identity network): partial sums per tile.
 struct AdjJob { const float *p; float *x; float scale; };
+struct AdjEi {
+    const float *x2;  // [B][n][n]
+    float *part;      // [B][adj_ei_part_floats / B]
+    unsigned *ctr;    // completion counter, zero before the launch (self-resetting)
+    float *out;       // ei [B]
+};
+size_t adj_ei_part_floats(const skei_plan *plan, int B);
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
-                             const int32_t *idx, int m, int idx_stride, cudaStream_t s);
+                             const int32_t *idx, int m, int idx_stride, cudaStream_t s,
+                             const AdjEi *ei = nullptr);
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s);
@@ -86,6 +118,15 @@ int host_draw(uint64_t seed, uint64_t iter, uint64_t image, int n_full, int m, i
               int32_t *g, int32_t *idx);
 
 // Batch grouping: images sharing one angle list are processed together in groups of bb.
+// Image group of the forward projector (same rule as pick_bb; kept separate because the
+// packed input layout depends on it).
+inline int fwd_bb(int B, int idx_stride) {
+    if (idx_stride != 0) return 1;
+    if (B % 4 == 0) return 4;
+    if (B % 2 == 0) return 2;
+    return 1;
+}
+
 inline int pick_bb(int B, int idx_stride) {
     if (idx_stride != 0) return 1;
     if (B % 4 == 0) return 4;

@@ -2,38 +2,46 @@
 // projector (BASELINE.json north_star: "radon_adj is its exact transpose, a per-pixel
 // gather over angles with the sketched angle table in shared memory").
 //
-// Design (DESIGN.md §5 "radon_adj"):
-//   * one CTA = a 32x32 pixel tile x BB images that share one angle list (BB = 4 for a
-//     per-pass sketch, 1 for per-image sketches) x one job (two jobs — FBP of q and the
-//     gradient of r — share a launch);
-//   * angles are processed in chunks of KC; for each angle the CTA stages the W-bin
-//     detector window the tile projects onto, interleaved over the BB images
-//     ([angle][bin][image], 16-byte rows for BB = 4), zero outside [0, n_det) so
-//     dropped taps need no branch;
-//   * each thread owns one column x 4 rows of the tile; per (pixel, angle) it forms
-//     j + f = t - s_0 in split precision (fp64 tile base per angle, fp32 local offset
-//     |.| < 48 px — DESIGN.md §5 "precision"), then 2 LDS.128 + 2*BB FFMA:
-//     acc_b += (1-f) q_b[j] + f q_b[j+1];
-//   * 8 lanes of a quarter-warp are 8 consecutive columns whose bins span <= 8
-//     consecutive 16-byte slots, so the LDS.128s are bank-conflict-free.
-// Work per (pixel, angle, image) = 2 taps, 8 bytes of shared-memory reads: this
-// kernel is bound by shared-memory bandwidth (the "gather roofline").
+// Design (DESIGN.md §7 "k_radon_adj"):
+//   * One CTA = a 32 x 32 pixel tile x BB images sharing one angle list x all jobs of the
+//     launch (the pass runs the FBP of q and the MC gradient of r as two jobs: they share
+//     the geometry, so it is computed once for 2*BB images).
+//   * Each thread owns two pairs of horizontally adjacent pixels (c, c+1) of one row.  The
+//     detector positions t and t + cos(th) of a pair lie within one 3-bin window [j, j+3),
+//     so a pair reads 3 bins per job (not 4) and interpolates each pixel with the 3 hat
+//     weights max(0, 1 - |t - j - k|) (one of which is 0).
+//   * Angles are processed in chunks of KC.  For each angle the CTA stages the W-bin detector
+//     window of the tile, interleaved [bin][image] (one LDS.128 = a bin of 4 images), zero
+//     outside [0, n_det) so dropped taps need no branch; chunks are double-buffered with
+//     cp.async so the next chunk's loads overlap this chunk's gathers.
+//   * Bank-conflict-free gathers: the 8 lanes of a shared-memory phase are 8 consecutive rows
+//     of one pixel column pair; their bins move by |sin th| <= 1 per row, so they span <= 8
+//     consecutive 16-byte slots (distinct banks, equal slots broadcast).
+//   * Positions in split precision: the fp64 tile-origin position per angle plus an fp32
+//     local offset < 48 px.
+//   * Optional fused epilogue (skei_pass with the identity network): ei partial sums
+//     sum (x2 - x_fbp)^2 per tile and image, reduced in fixed order by the last CTA.
+// Work per (pixel, angle, image) = 2 taps; per pixel pair and angle 3 LDS.BB per job.
 #include "internal.h"
 
 namespace skei {
 namespace {
 
-constexpr int kTile = 32;        // tile side (pixels)
-constexpr int kRowsPerThread = 4;
-constexpr int kThreads = 256;    // 32 columns x 8 row groups
-constexpr int kKC = 32;          // angles per staged chunk
-constexpr int kW = 48;           // staged bins per angle (>= 31*sqrt(2) + 3)
+constexpr int kTile = 32;      // tile side (pixels)
+constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 16 columns
+constexpr int kKC = 12;        // angles per staged chunk (2 buffers x 2 jobs fit 48 KB)
+constexpr int kW = 48;         // staged bins per angle (>= 31 sqrt 2 + 3)
 
 struct AdjArgs {
     AdjJob job[2];
     const int32_t *idx;
     int m, idx_stride, B, tiles_x;
     Geom g;
+    // fused ei epilogue (job 0 = FBP): x2 [B][n][n], partials [B][ntiles], counter, ei [B]
+    const float *ei_x2;
+    float *ei_part;
+    unsigned *ei_ctr;
+    float *ei_out;
 };
 
 template <int BB>
@@ -43,102 +51,237 @@ template <> struct Vec<2> { using T = float2; };
 template <> struct Vec<4> { using T = float4; };
 
 template <int BB>
-__device__ inline void load_bins(const float *base, float (&v)[BB]) {
+__device__ __forceinline__ void load_bins(const float *base, float (&v)[BB]) {
     typename Vec<BB>::T t = *reinterpret_cast<const typename Vec<BB>::T *>(base);
     const float *pt = reinterpret_cast<const float *>(&t);
 #pragma unroll
     for (int b = 0; b < BB; ++b) v[b] = pt[b];
 }
 
-template <int BB>
-__global__ void __launch_bounds__(kThreads) k_radon_adj(AdjArgs a) {
-    __shared__ __align__(16) float win[kKC * kW * BB];
-    __shared__ float s_off[kKC], s_cos[kKC], s_sin[kKC];
-    __shared__ int s_w0[kKC], s_slot[kKC];
+__device__ __forceinline__ void cp_async4(float *smem, const float *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
 
-    const AdjJob job = blockIdx.z ? a.job[1] : a.job[0];
+// hat weights of a position u in [0, 2] against bins 0, 1, 2
+__device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
+    w0 = fmaxf(0.f, 1.f - u);
+    w1 = 1.f - fabsf(u - 1.f);
+    w2 = fmaxf(0.f, u - 1.f);
+}
+
+template <int BB, int NJ>
+__global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
+    __shared__ __align__(16) float win[2][NJ][kKC * kW * BB];
+    __shared__ float s_off[2][kKC], s_cos[2][kKC], s_sin[2][kKC];
+    __shared__ int s_w0[2][kKC];
+    __shared__ float s_red[kThreads / 32][BB];
+    __shared__ bool s_last;
+
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
     const int tr0 = (tile / a.tiles_x) * kTile, tc0 = (tile % a.tiles_x) * kTile;
     const int b0 = blockIdx.y * BB;
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp w: rows 8*(w/2) .. +7, columns 16*(w%2) .. +15; lane: row (lane % 8), pair
+    // columns (lane / 8) and (lane / 8) + 4 of the warp's 8 pairs
+    const int ry = 8 * (warp >> 1) + (lane & 7);
+    const int pc0 = 8 * (warp & 1) + (lane >> 3);  // pair index 0..15, second pair = +4
     const long nn = (long)n * n;
 
-    float acc[kRowsPerThread][BB];
+    float acc[NJ][2][2][BB];  // [job][pair][pixel][image]
 #pragma unroll
-    for (int i = 0; i < kRowsPerThread; ++i)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int b = 0; b < BB; ++b) acc[i][b] = 0.f;
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int b = 0; b < BB; ++b) acc[j][p][q][b] = 0.f;
 
-    for (int k0 = 0; k0 < a.m; k0 += kKC) {
+    const int nchunks = (a.m + kKC - 1) / kKC;
+    // per-angle table + window staging of chunk ch into buffer bf
+    auto stage = [&](int ch, int bf) {
+        const int k0 = ch * kKC;
         const int kc = min(kKC, a.m - k0);
-        if (threadIdx.x < kc) {
-            const int k = k0 + threadIdx.x;
-            const double2 cs = a.g.trig[idx[k]];
-            // jpos at the tile origin pixel (tr0, tc0), fp64
-            const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
-            const double jmin = J0 + fmin(0.0, (kTile - 1) * cs.x) + fmin(0.0, -(kTile - 1) * cs.y);
-            const double w0 = floor(jmin);
-            s_off[threadIdx.x] = (float)(J0 - w0);
-            s_cos[threadIdx.x] = (float)cs.x;
-            s_sin[threadIdx.x] = (float)cs.y;
-            s_w0[threadIdx.x] = (int)w0;
-            s_slot[threadIdx.x] = k;
+        if (threadIdx.x < kKC) {
+            if (threadIdx.x < kc) {
+                const double2 cs = a.g.trig[idx[k0 + threadIdx.x]];
+                // detector position of the tile origin pixel (tr0, tc0), fp64
+                const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
+                const double jmin =
+                    J0 + fmin(0.0, (kTile - 1) * cs.x) + fmin(0.0, -(kTile - 1) * cs.y);
+                const double w0 = floor(jmin);
+                s_off[bf][threadIdx.x] = (float)(J0 - w0);
+                s_cos[bf][threadIdx.x] = (float)cs.x;
+                s_sin[bf][threadIdx.x] = (float)cs.y;
+                s_w0[bf][threadIdx.x] = (int)w0;
+            }
         }
-        __syncthreads();
-        // stage windows: element e -> (angle t, bin w, image b), image fastest
+        __syncthreads();  // window origins visible
+        // element e -> (angle t, bin w, image b), image fastest; zero outside [0, n_det)
         for (int e = threadIdx.x; e < kc * kW * BB; e += kThreads) {
             const int b = e % BB;
             const int w = (e / BB) % kW;
             const int t = e / (BB * kW);
-            const int j = s_w0[t] + w;
-            float v = 0.f;
-            if (j >= 0 && j < n_det)
-                v = __ldg(job.p + ((long)(b0 + b) * a.m + s_slot[t]) * n_det + j);
-            win[e] = v;
+            const int jb = s_w0[bf][t] + w;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                float *dst = &win[bf][jj][e];
+                if (jb >= 0 && jb < n_det)
+                    cp_async4(dst, a.job[jj].p + ((long)(b0 + b) * a.m + k0 + t) * n_det + jb);
+                else
+                    *dst = 0.f;
+            }
+        }
+        cp_async_commit();
+    };
+
+    stage(0, 0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int bf = ch & 1;
+        if (ch + 1 < nchunks) {
+            stage(ch + 1, bf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        const int kc = min(kKC, a.m - ch * kKC);
 #pragma unroll 2
         for (int t = 0; t < kc; ++t) {
-            const float ct = s_cos[t], st = s_sin[t];
-            const float base = fmaf((float)tx, ct, fmaf(-(float)ty, st, s_off[t]));
-            const float step = -8.0f * st;
-            const float *wt = win + t * kW * BB;
+            const float ct = s_cos[bf][t], st = s_sin[bf][t];
+            // position of pixel (ry, 2 pc) relative to the window origin
+            const float rowb = fmaf(-(float)ry, st, s_off[bf][t]);
 #pragma unroll
-            for (int i = 0; i < kRowsPerThread; ++i) {
-                float jr = fmaxf(fmaf((float)i, step, base), 0.f);
-                const float fl = floorf(jr);
-                const float f = jr - fl;
-                const int j = min((int)fl, kW - 2);
-                float q0[BB], q1[BB];
-                load_bins<BB>(wt + j * BB, q0);
-                load_bins<BB>(wt + (j + 1) * BB, q1);
-                const float f0 = 1.f - f;
+            for (int p = 0; p < 2; ++p) {
+                const int c = 2 * (pc0 + 4 * p);
+                const float t1 = fmaf((float)c, ct, rowb);
+                const float t2 = t1 + ct;
+                const float lo = fmaxf(fminf(t1, t2), 0.f);
+                const float jf = floorf(lo);
+                const int j = min((int)jf, kW - 3);
+                const float u1 = t1 - (float)j, u2 = t2 - (float)j;
+                float w10, w11, w12, w20, w21, w22;
+                hat3(u1, w10, w11, w12);
+                hat3(u2, w20, w21, w22);
 #pragma unroll
-                for (int b = 0; b < BB; ++b) acc[i][b] = fmaf(f, q1[b], fmaf(f0, q0[b], acc[i][b]));
+                for (int jj = 0; jj < NJ; ++jj) {
+                    const float *wt = &win[bf][jj][(t * kW + j) * BB];
+                    float q0[BB], q1[BB], q2[BB];
+                    load_bins<BB>(wt, q0);
+                    load_bins<BB>(wt + BB, q1);
+                    load_bins<BB>(wt + 2 * BB, q2);
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) {
+                        acc[jj][p][0][b] =
+                            fmaf(w12, q2[b], fmaf(w11, q1[b], fmaf(w10, q0[b], acc[jj][p][0][b])));
+                        acc[jj][p][1][b] =
+                            fmaf(w22, q2[b], fmaf(w21, q1[b], fmaf(w20, q0[b], acc[jj][p][1][b])));
+                    }
+                }
             }
         }
-        __syncthreads();
+        __syncthreads();  // buffer bf is free for chunk ch + 2
     }
-    const int c = tc0 + tx;
-    if (c < n) {
+
+    // ---- epilogue: scale and store; optional fused ei partials (job 0 = FBP)
+    const int r = tr0 + ry;
+    float eacc[BB];
 #pragma unroll
-        for (int i = 0; i < kRowsPerThread; ++i) {
-            const int r = tr0 + ty + 8 * i;
-            if (r < n) {
+    for (int b = 0; b < BB; ++b) eacc[b] = 0.f;
 #pragma unroll
-                for (int b = 0; b < BB; ++b)
-                    job.x[(long)(b0 + b) * nn + (long)r * n + c] = job.scale * acc[i][b];
+    for (int jj = 0; jj < NJ; ++jj) {
+        const float sc = a.job[jj].scale;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int c = tc0 + 2 * (pc0 + 4 * p);
+            if (r >= n) continue;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                const long o = (long)(b0 + b) * nn + (long)r * n + c;
+                const float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
+                if (c + 1 < n && ((o & 1) == 0)) {
+                    *reinterpret_cast<float2 *>(a.job[jj].x + o) = make_float2(v0, v1);
+                } else {
+                    if (c < n) a.job[jj].x[o] = v0;
+                    if (c + 1 < n) a.job[jj].x[o + 1] = v1;
+                }
+                if (jj == 0 && a.ei_x2) {
+                    if (c < n) {
+                        const float d = __ldg(a.ei_x2 + o) - v0;
+                        eacc[b] = fmaf(d, d, eacc[b]);
+                    }
+                    if (c + 1 < n) {
+                        const float d = __ldg(a.ei_x2 + o + 1) - v1;
+                        eacc[b] = fmaf(d, d, eacc[b]);
+                    }
+                }
             }
         }
     }
+    if (!a.ei_x2) return;
+    // deterministic per-tile partial per image, then the last CTA sums the tiles in order
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+        float v = eacc[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_red[warp][b] = v;
+    }
+    __syncthreads();
+    const int ntiles = gridDim.x;
+    if (threadIdx.x < BB) {
+        float v = 0.f;
+        for (int w = 0; w < kThreads / 32; ++w) v += s_red[w][threadIdx.x];
+        a.ei_part[(long)(b0 + threadIdx.x) * ntiles + tile] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned total = gridDim.x * gridDim.y;
+        s_last = atomicAdd(a.ei_ctr, 1u) == total - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // the last CTA: ei[b] = sum over tiles in tile order, fp64, one warp per image
+    for (int b = warp; b < a.B; b += kThreads / 32) {
+        double s = 0.0;
+        for (int i = lane; i < ntiles; i += 32) s += (double)__ldcg(a.ei_part + (long)b * ntiles + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) a.ei_out[b] = (float)s;
+    }
+    if (threadIdx.x == 0) *a.ei_ctr = 0u;  // ready for the next launch
+}
+
+template <int BB>
+cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
+    dim3 grid((unsigned)(a.tiles_x * a.tiles_x), (unsigned)(B / BB), 1);
+    if (njobs == 2)
+        k_radon_adj<BB, 2><<<grid, kThreads, 0, s>>>(a);
+    else
+        k_radon_adj<BB, 1><<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
+size_t adj_ei_part_floats(const skei_plan *plan, int B) {
+    const int t = (plan->n + kTile - 1) / kTile;
+    return (size_t)B * t * t;
+}
+
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
-                             const int32_t *idx, int m, int idx_stride, cudaStream_t s) {
+                             const int32_t *idx, int m, int idx_stride, cudaStream_t s,
+                             const AdjEi *ei) {
     AdjArgs a;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
@@ -148,14 +291,16 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
     a.B = B;
     a.g = geom_of(plan);
     a.tiles_x = (plan->n + kTile - 1) / kTile;
+    a.ei_x2 = ei ? ei->x2 : nullptr;
+    a.ei_part = ei ? ei->part : nullptr;
+    a.ei_ctr = ei ? ei->ctr : nullptr;
+    a.ei_out = ei ? ei->out : nullptr;
     const int bb = pick_bb(B, idx_stride);
-    dim3 grid((unsigned)(a.tiles_x * a.tiles_x), (unsigned)(B / bb), (unsigned)njobs);
     switch (bb) {
-        case 4: k_radon_adj<4><<<grid, kThreads, 0, s>>>(a); break;
-        case 2: k_radon_adj<2><<<grid, kThreads, 0, s>>>(a); break;
-        default: k_radon_adj<1><<<grid, kThreads, 0, s>>>(a); break;
+        case 4: return launch_bb<4>(a, njobs, B, s);
+        case 2: return launch_bb<2>(a, njobs, B, s);
+        default: return launch_bb<1>(a, njobs, B, s);
     }
-    return cudaGetLastError();
 }
 
 }  // namespace skei

@@ -16,17 +16,20 @@
 //     double-buffered, issued by one thread: no staging instructions, no registers) and one
 //     LDS.BB fetches a candidate pixel of BB images.
 //   * Work unit = (job, group of BB images sharing the sketch, class, group of K angles);
-//     the S CTAs of a thread-block cluster (S chosen at launch to fill the waves) split the
-//     unit's lines.  Staged pixels are reused by all K angles of the unit.
+//     the S CTAs of a thread-block cluster split the unit's lines.  Staged pixels are reused
+//     by all K angles of the unit.  The kernel is persistent: one cluster per S SMs loops
+//     over the non-empty units (class sizes are counted on the device), and the block
+//     stream continues across units, so the next unit's first blocks are in flight while
+//     the current unit's epilogue runs.
 //   * Bank-conflict-free gathers: lane L processes the lines of a block in the skewed
 //     order l = (L + s) mod R.  The lanes of one shared-memory phase (8 lanes for LDS.128,
 //     16 for LDS.64, 32 for LDS.32) then read R distinct line slots, i.e. distinct banks,
 //     whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way conflicts at
 //     every angle with |beta| < 1 because 8 bins span more than 8 pixels).
-//   * 1024 threads (64 registers each), one CTA per SM.  Task = (angle, 32 consecutive
+//   * 512 threads (128 registers each), one CTA per SM.  Task = (angle, 32 consecutive
 //     bins), lane = bin; the K x chunks tasks are dealt round-robin to the 32 warps (each
 //     warp gets a mix of angles, whose footprints differ); a thread owns up to kMaxT tasks
-//     and keeps BB accumulators per task in registers: K = 32 kMaxT / chunks angles.
+//     and keeps BB accumulators per task in registers: K = 16 kMaxT / chunks angles.
 //   * Decoupled pipeline: no per-block barrier.  The last warp to finish a staged block
 //     (shared-memory counter) refills its buffer with the block nbuf ahead, so warps drift
 //     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
@@ -35,9 +38,13 @@
 //     is 0), 3*BB FFMA.  The R lines of a block are summed into a partial before it is
 //     added to the running total (two-level summation).  A chunk skips a block none of its
 //     32 bins sees.
-//   * End: per-CTA partial projections -> shared memory -> fixed-rank-order sum across the
-//     cluster through distributed shared memory (deterministic, no atomics) -> p.
+//   * Unit end: per-CTA partial projections -> shared memory -> fixed-rank-order sum across
+//     the cluster through distributed shared memory (deterministic, no atomics) -> p; for
+//     the MC job also r = p - y_S and per-(unit, rank) partial sums of r^2, summed in a
+//     fixed order by the last CTA to finish (completion counter).
 #include <cooperative_groups.h>
+
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -46,23 +53,34 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxT = 6;    // 32-bin chunks per thread (registers left for load pipelining)
-constexpr int kKMax = 32;   // angles per CTA
+constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
+// 32-bin tasks per thread: accumulators = kMaxT * BB registers of the 64 available
+template <int BB>
+constexpr int max_tasks() { return 6; }
+constexpr int kKMax = 16;   // angles per CTA
 constexpr int kPadL = 4;    // zero pixel columns left of the line data
 constexpr int kPadR = 4;    // ... and right of it (candidates reach n + 2)
 constexpr int kColF = 32;   // floats per staged pixel column (R * BB)
 
 struct FwdArgs {
     FwdJob job[2];
+    int njobs;
     const int32_t *idx;
-    int m, idx_stride, B;
-    int K;       // angles per CTA: K * chunks <= kWarps * kMaxT tasks
+    int m, idx_stride, B, nq;  // nq = image groups = B / BB
+    int K;       // angles per unit: K * chunks <= kWarps * kMaxT tasks
     int chunks;  // ceil(n_det / 32)
     int nblk;    // packed blocks per image group (ceil(n / R))
-    int nbuf;    // staging buffers (2 = double-buffered)
+    int nbuf;    // staging buffers
     Geom g;
+    // fused MC residual of job 0 (job.y != NULL): partials [B][mc_slots], counter, mc [B]
+    float *mc_part;
+    int mc_slots;
+    unsigned *mc_ctr;
+    float *mc_out;
+    unsigned *queue;  // work-queue counter (zero before the launch)
+    float *scratch;   // per-CTA partial projections [gridDim.x][K * n_det * BB]
 };
 
 // ---- TMA bulk copy + mbarrier (sm_90+ async proxy), inline PTX
@@ -120,89 +138,109 @@ template <> struct Px<1> { using T = float; };
 template <> struct Px<2> { using T = float2; };
 template <> struct Px<4> { using T = float4; };
 
+// ld.shared of one staged pixel of BB images at a 32-bit shared-window address
 template <int BB>
-__device__ __forceinline__ void ld_px(const float *p, float (&v)[BB]) {
-    const typename Px<BB>::T t = *reinterpret_cast<const typename Px<BB>::T *>(p);
-    const float *pt = reinterpret_cast<const float *>(&t);
-#pragma unroll
-    for (int b = 0; b < BB; ++b) v[b] = pt[b];
+__device__ __forceinline__ void lds_px(unsigned addr, float (&v)[BB]) {
+    if constexpr (BB == 4) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                     : "r"(addr));
+    } else if constexpr (BB == 2) {
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(v[0]), "=f"(v[1]) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[0]) : "r"(addr));
+    }
+}
+
+// L2 (ld.global.cg) load of BB consecutive floats (16-byte aligned for BB = 4)
+template <int BB>
+__device__ __forceinline__ void ldcg_vec(const float *p, float (&v)[BB]) {
+    if constexpr (BB == 4) {
+        const float4 t = __ldcg(reinterpret_cast<const float4 *>(p));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else if constexpr (BB == 2) {
+        const float2 t = __ldcg(reinterpret_cast<const float2 *>(p));
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = __ldcg(p);
+    }
+}
+
+// Work decomposition shared by every CTA: for each image group q, nrow[q] = angles of its
+// sketch in the row class; units of q = ceil(nrow/K) + ceil((m - nrow)/K); uoff = prefix.
+struct Units {
+    const int *uoff;  // [nq + 1]
+    const int *nrow;  // [nq]
+    int per_job;      // uoff[nq]
+};
+struct UnitId {
+    int job, q, cls, grp;
+};
+__device__ __forceinline__ UnitId decode_unit(const Units &U, int nq, int K, int u) {
+    UnitId d;
+    d.job = u / U.per_job;
+    const int rem = u - d.job * U.per_job;
+    int lo = 0, hi = nq - 1;  // last q with uoff[q] <= rem
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (U.uoff[mid] <= rem) lo = mid; else hi = mid - 1;
+    }
+    d.q = lo;
+    const int gi = rem - U.uoff[lo];
+    const int gr = (U.nrow[lo] + K - 1) / K;
+    d.cls = gi < gr ? 0 : 1;
+    d.grp = d.cls ? gi - gr : gi;
+    return d;
 }
 
 template <int BB>
 __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     constexpr int R = kColF / BB;
-    extern __shared__ __align__(128) float smem[];  // nbuf x [n + pads][R][BB]; partials at end
+    constexpr int kMaxT = max_tasks<BB>();
+    extern __shared__ __align__(128) float smem[];  // nbuf stage buffers
     __shared__ __align__(8) uint64_t full[3];
     __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
     __shared__ float sAbsB[kKMax], sSec[kKMax], sPlf[kKMax];
     __shared__ int sSlot[kKMax];
     __shared__ int sCount;
+    __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
+    __shared__ float s_red[kWarps][BB];
+    __shared__ bool s_last;
+    __shared__ int s_units[4];  // ring of this cluster's next units (grabbed one unit ahead)
 
     cg::cluster_group cluster = cg::this_cluster();
     const int S = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
-    const int unit = blockIdx.x / S;
-    const int cls = unit & 1, grp = unit >> 1;
-    const FwdJob job = blockIdx.z ? a.job[1] : a.job[0];
-    const int b0 = blockIdx.y * BB;
-    const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
+    const int cid = blockIdx.x / S, ncl = gridDim.x / S;
     const int n = a.g.n, n_det = a.g.n_det, n_full = a.g.n_full;
-    const int K = a.K;
+    const int K = a.K, nq = a.nq;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int stage_f = (n + kPadL + kPadR) * kColF;
+    const long part_f = (long)K * n_det * BB;
+    float *part = a.scratch + (long)blockIdx.x * part_f;  // this CTA's partials (L2)
 
-    // ---- 1. the grp-th group of K angles of class cls, in sketch-slot order
-    if (threadIdx.x < 32) {
-        int seen = 0;
+    // ---- 1. class sizes per image group -> unit table (identical in every CTA)
+    for (int q = warp; q < nq; q += kWarps) {
+        const int32_t *iq = a.idx + (a.idx_stride ? (long)q * BB * a.idx_stride : 0);
+        int cnt = 0;
         for (int base = 0; base < a.m; base += 32) {
             const int k = base + lane;
-            bool in = false;
+            bool row = false;
             if (k < a.m) {
-                const int i = idx[k];
-                const bool row_class = (4 * i <= n_full) || (4 * i >= 3 * n_full);
-                in = (cls == 0) ? row_class : !row_class;
+                const int i = iq[k];
+                row = (4 * i <= n_full) || (4 * i >= 3 * n_full);
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, in);
-            const int pre = seen + __popc(bal & ((1u << lane) - 1u));
-            if (in && pre >= grp * K && pre < grp * K + K) sSlot[pre - grp * K] = k;
-            seen += __popc(bal);
+            cnt += __popc(__ballot_sync(0xffffffffu, row));
         }
-        if (lane == 0) sCount = max(0, min(K, seen - grp * K));
+        if (lane == 0) s_nrow[q] = cnt;
     }
-    __syncthreads();
-    const int kcnt = sCount;
-    if (kcnt == 0) return;  // same decision in every CTA of the cluster (depends on unit only)
-
-    // ---- 2. per-angle line geometry in fp64: a*(j, l) = P0 + j Pj + l Pl
-    if (threadIdx.x < kcnt) {
-        const double2 cs = a.g.trig[idx[sSlot[threadIdx.x]]];
-        const double c = cs.x, s = cs.y, h = a.g.h, hd = a.g.hd;
-        double P0, Pj, Pl, ab;
-        if (cls == 0) {  // lines = rows r, along = columns: c* = h + (j - hd - (h - r) s)/c
-            P0 = h - (hd + h * s) / c;
-            Pj = 1.0 / c;
-            Pl = s / c;
-            ab = fabs(c);
-        } else {  // lines = columns c, along = rows: r* = h + (hd - j + (c - h) cos)/sin
-            P0 = h + (hd - h * c) / s;
-            Pj = -1.0 / s;
-            Pl = c / s;
-            ab = fabs(s);
-        }
-        sP0[threadIdx.x] = P0;
-        sPj[threadIdx.x] = Pj;
-        sPl[threadIdx.x] = Pl;
-        sAbsB[threadIdx.x] = (float)ab;
-        sSec[threadIdx.x] = (float)(1.0 / ab);
-        sPlf[threadIdx.x] = (float)Pl;
-    }
-    // zero pad columns of every buffer (never written by the bulk copies)
-    const int stage_f = (n + kPadL + kPadR) * kColF;
+    // zero pad columns of every stage buffer (never written by the bulk copies)
     for (int e = threadIdx.x; e < a.nbuf * (kPadL + kPadR) * kColF; e += kThreads) {
         const int bi = e / ((kPadL + kPadR) * kColF);
         const int e2 = e - bi * (kPadL + kPadR) * kColF;
-        const int q = e2 / kColF, w = e2 - q * kColF;
-        const int col = q < kPadL ? q : kPadL + n + (q - kPadL);
+        const int qq = e2 / kColF, w = e2 - qq * kColF;
+        const int col = qq < kPadL ? qq : kPadL + n + (qq - kPadL);
         smem[bi * stage_f + col * kColF + w] = 0.f;
     }
     if (threadIdx.x == 0) {
@@ -213,170 +251,373 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         fence_mbar_init();
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc_u = 0;
+        for (int q = 0; q < nq; ++q) {
+            s_uoff[q] = acc_u;
+            acc_u += (s_nrow[q] + K - 1) / K + (a.m - s_nrow[q] + K - 1) / K;
+        }
+        s_uoff[nq] = acc_u;
+    }
+    __syncthreads();
+    const Units U{s_uoff, s_nrow, s_uoff[nq]};
+    const int total_units = a.njobs * U.per_job;
+    // dynamic unit queue: the cluster leader grabs units (global counter) one unit ahead and
+    // the other ranks read them through DSMEM after the cluster barriers
+    if (rank == 0 && threadIdx.x == 0) {
+        s_units[0] = (int)atomicAdd(a.queue, 1u);
+        s_units[1] = (int)atomicAdd(a.queue, 1u);
+    }
+    cluster.sync();
+    if (rank != 0 && threadIdx.x < 2) s_units[threadIdx.x] = cluster.map_shared_rank(s_units, 0)[threadIdx.x];
+    __syncthreads();
 
-    // this CTA's lines: whole packed blocks
+    // this CTA's lines: the same whole packed blocks in every unit
     const int blocks_per = (a.nblk + S - 1) / S;
     const int blk0 = min(a.nblk, rank * blocks_per), blk1 = min(a.nblk, blk0 + blocks_per);
     const int nb = blk1 - blk0;
-    const float *xsrc = (cls ? job.xc : job.xr) + (long)blockIdx.y * a.nblk * n * kColF;
-    // TMA pipeline: block q lives in buffer q % nbuf.  Blocks 0..nbuf-1 are issued up front;
-    // block q + nbuf is issued by the last warp to finish block q (shared counter), so warps
-    // are never barrier-synchronised per block and can drift up to nbuf - 1 blocks apart.
-    const int nbuf = a.nbuf;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < min(nbuf, nb); ++q)
-            issue_block(smem + q * stage_f + kPadL * kColF, xsrc + (long)(blk0 + q) * n * kColF, n,
-                        &full[q]);
+    // this CTA's block stream: block g belongs to local unit g / nb; it exists if that unit
+    // is known (at most one unit ahead) and valid
+    auto block_ok = [&](int g) -> bool {
+        return nb > 0 && s_units[(g / nb) & 3] < total_units;
+    };
+    auto block_src = [&](int g) -> const float * {
+        const int iu = g / nb, i = g - iu * nb;
+        const UnitId d = decode_unit(U, nq, K, s_units[iu & 3]);
+        const FwdJob &jb = d.job ? a.job[1] : a.job[0];
+        return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + blk0 + i) * n * kColF;
+    };
+    // TMA pipeline: block g lives in buffer g % nbuf; blocks 0..nbuf-1 are issued up front,
+    // block g + nbuf by the last warp to finish block g (shared counter), so warps are not
+    // barrier-synchronised per block and the stream runs on across unit boundaries (at
+    // most one unit ahead, hence nbuf <= nb).
+    const int nbuf = max(1, min(a.nbuf, nb));
+    if (threadIdx.x == 0)
+        for (int g = 0; g < nbuf && g < 2 * nb && block_ok(g); ++g)
+            issue_block(smem + g * stage_f + kPadL * kColF, block_src(g), n, &full[g]);
+
+    // this lane's skewed line order l_s = (lane + s) mod R, as a float (position) and as a
+    // byte offset within a staged pixel column (minus 3 pad columns, see the clamp below)
+    float lfs[R];
+    unsigned lofs[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+        const int l = (lane + s) & (R - 1);
+        lfs[s] = (float)l;
+        lofs[s] = (unsigned)(((kPadL - 3) * kColF + l * BB) * sizeof(float));
     }
-
-    // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps, so every
-    // warp holds a mix of angles (near-0 and near-45 degree angles have different footprints)
-    const int ntask = kcnt * a.chunks;
+    const unsigned smem_b = smem_u32(smem);
+    const unsigned cmax = (unsigned)(n + 3);
     const float fn1 = (float)(n - 1);
-    float acc[kMaxT][BB];
-#pragma unroll
-    for (int t = 0; t < kMaxT; ++t)
-#pragma unroll
-        for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
 
-    for (int i = 0; i < nb; ++i) {
-        const int lb = (blk0 + i) * R;
-        const int cb = i % nbuf;
-        const float *cur = smem + cb * stage_f;
-        mbar_wait(&full[cb], (unsigned)((i / nbuf) & 1));
+    for (int iu = 0;; ++iu) {
+        const int u = s_units[iu & 3];
+        if (u >= total_units) break;  // same in every CTA of the cluster
+        const UnitId d = decode_unit(U, nq, K, u);
+        const FwdJob job = d.job ? a.job[1] : a.job[0];
+        const int b0 = d.q * BB;
+        const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
+
+        // ---- 2. the unit's K angles (grp-th group of class cls, sketch-slot order) + geometry
+        if (warp == 0) {
+            int seen = 0;
+            for (int base = 0; base < a.m; base += 32) {
+                const int k = base + lane;
+                bool in = false;
+                if (k < a.m) {
+                    const int i = idx[k];
+                    const bool row_class = (4 * i <= n_full) || (4 * i >= 3 * n_full);
+                    in = (d.cls == 0) ? row_class : !row_class;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pre = seen + __popc(bal & ((1u << lane) - 1u));
+                if (in && pre >= d.grp * K && pre < d.grp * K + K) sSlot[pre - d.grp * K] = k;
+                seen += __popc(bal);
+            }
+            if (lane == 0) sCount = max(0, min(K, seen - d.grp * K));
+            __syncwarp();
+            if (lane < min(K, max(0, seen - d.grp * K))) {
+                const double2 cs = a.g.trig[idx[sSlot[lane]]];
+                const double c = cs.x, sn = cs.y, h = a.g.h, hd = a.g.hd;
+                double P0, Pj, Pl, ab;
+                if (d.cls == 0) {  // lines = rows r, along = columns
+                    P0 = h - (hd + h * sn) / c;
+                    Pj = 1.0 / c;
+                    Pl = sn / c;
+                    ab = fabs(c);
+                } else {  // lines = columns c, along = rows
+                    P0 = h + (hd - h * c) / sn;
+                    Pj = -1.0 / sn;
+                    Pl = c / sn;
+                    ab = fabs(sn);
+                }
+                sP0[lane] = P0;
+                sPj[lane] = Pj;
+                sPl[lane] = Pl;
+                sAbsB[lane] = (float)ab;
+                sSec[lane] = (float)(1.0 / ab);
+                sPlf[lane] = (float)Pl;
+            }
+        }
+        __syncthreads();
+        const int kcnt = sCount;
+        const int ntask = kcnt * a.chunks;
+
+        // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps
+        int tk[kMaxT], tj[kMaxT];  // angle slot and bin of this lane's tasks (tk < 0: none)
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t) {
             const int tau = warp + kWarps * t;
-            if (tau >= ntask) break;  // warp-uniform
-            const int k = tau / a.chunks;
-            const int chunk = tau - k * a.chunks;
-            const int j = chunk * 32 + lane;
-            const double Pl = sPl[k];
-            const double ad = sP0[k] + (double)lb * Pl + (double)j * sPj[k];
-            const double fl = floor(ad);
-            const int base = (int)fl;
-            const float frac = (float)(ad - fl);
-            const float ab = sAbsB[k], sec = sSec[k], plf = sPlf[k];
-            // does any bin of this chunk see a line of this block?
-            const float span = (float)(R - 1) * plf;
-            const float lo = (float)base + frac + fminf(0.f, span);
-            const float hi = (float)base + frac + fmaxf(0.f, span);
-            const bool act = j < n_det && hi + sec > 0.f && lo - sec < fn1;
-            if (!__any_sync(0xffffffffu, act)) continue;
-            const float c1 = 2.f * ab - 1.f, c2 = 2.f - 3.f * ab;
-            const float fs = frac - sec;
-            float blk[BB];
+            tk[t] = tau < ntask ? tau / a.chunks : -1;
+            tj[t] = tau < ntask ? (tau - tk[t] * a.chunks) * 32 + lane : 0;
+        }
+        float acc[kMaxT][BB];
 #pragma unroll
-            for (int b = 0; b < BB; ++b) blk[b] = 0.f;
+        for (int t = 0; t < kMaxT; ++t)
 #pragma unroll
-            for (int s = 0; s < R; ++s) {
-                const int l = (lane + s) & (R - 1);
-                // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
-                // phi = e - floor(e) the hat weights of the 3 candidates are
-                //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
-                const float e = fmaf((float)l, plf, fs);
-                const float fl2 = floorf(e);
-                const float phi = e - fl2;
-                int ci = base + (int)fl2 + 1;
-                ci = min(max(ci, -3), n);
-                const float w0 = fmaf(-ab, phi, ab);
-                const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
-                const float w2 = fmaf(ab, phi, c2);
-                const float *px = cur + (ci + kPadL) * kColF + l * BB;
-                float v0[BB], v1[BB], v2[BB];
-                ld_px<BB>(px, v0);
-                ld_px<BB>(px + kColF, v1);
+            for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
+
+        for (int i = 0; i < nb; ++i) {
+            const int g = iu * nb + i;
+            const int lb = (blk0 + i) * R;
+            const int cb = g % nbuf;
+            const unsigned cur_b = smem_b + (unsigned)(cb * stage_f * sizeof(float));
+            mbar_wait(&full[cb], (unsigned)((g / nbuf) & 1));
 #pragma unroll
-                for (int b = 0; b < BB; ++b) blk[b] = fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b]));
-                if (w2 > 0.f) {
-                    ld_px<BB>(px + 2 * kColF, v2);
+            for (int t = 0; t < kMaxT; ++t) {
+                const int k = tk[t];
+                if (k < 0) break;  // warp-uniform
+                const int j = tj[t];
+                const double Pl = sPl[k];
+                const double ad = sP0[k] + (double)lb * Pl + (double)j * sPj[k];
+                const double fl = floor(ad);
+                const int base = (int)fl;
+                const float frac = (float)(ad - fl);
+                const float ab = sAbsB[k], sec = sSec[k], plf = sPlf[k];
+                // does any bin of this chunk see a line of this block?
+                const float span = (float)(R - 1) * plf;
+                const float lo = (float)base + frac + fminf(0.f, span);
+                const float hi = (float)base + frac + fmaxf(0.f, span);
+                const bool act = j < n_det && hi + sec > 0.f && lo - sec < fn1;
+                if (!__any_sync(0xffffffffu, act)) continue;
+                const float c1 = 2.f * ab - 1.f, c2 = 2.f - 3.f * ab;
+                const float fs = frac - sec;
+                const int base4 = base + 4;
+                float blk[BB];
 #pragma unroll
-                    for (int b = 0; b < BB; ++b) blk[b] = fmaf(w2, v2[b], blk[b]);
+                for (int b = 0; b < BB; ++b) blk[b] = 0.f;
+#pragma unroll
+                for (int s = 0; s < R; ++s) {
+                    // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
+                    // phi = e - floor(e) the hat weights of the 3 candidates are
+                    //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
+                    const float e = fmaf(lfs[s], plf, fs);
+                    const float fl2 = floorf(e);
+                    const float phi = e - fl2;
+                    // candidate_0 + 3 clamped to [0, n + 3] in one unsigned min (lanes whose
+                    // bin misses the line land in the zero pad columns)
+                    const unsigned cu = min((unsigned)(base4 + (int)fl2), cmax);
+                    const float w0 = fmaf(-ab, phi, ab);
+                    const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
+                    const float w2 = fmaf(ab, phi, c2);
+                    const unsigned pa = cur_b + cu * (unsigned)(kColF * sizeof(float)) + lofs[s];
+                    float v0[BB], v1[BB], v2[BB];
+                    lds_px<BB>(pa, v0);
+                    lds_px<BB>(pa + kColF * sizeof(float), v1);
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) blk[b] = fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b]));
+                    if (w2 > 0.f) {
+                        lds_px<BB>(pa + 2 * kColF * sizeof(float), v2);
+#pragma unroll
+                        for (int b = 0; b < BB; ++b) blk[b] = fmaf(w2, v2[b], blk[b]);
+                    }
+                }
+#pragma unroll
+                for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
+            }
+            // release the buffer; the last warp out refills it with block g + nbuf
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();  // this warp's reads of the buffer are complete
+                const int old = atomicAdd(&done[cb], 1);
+                if (old == kWarps * (g / nbuf + 1) - 1 && (g + nbuf) / nb <= iu + 1 &&
+                    block_ok(g + nbuf)) {
+                    fence_proxy_async();  // generic-proxy reads -> async-proxy writes
+                    issue_block(smem + cb * stage_f + kPadL * kColF, block_src(g + nbuf), n,
+                                &full[cb]);
                 }
             }
-#pragma unroll
-            for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
         }
-        // release the buffer; the last warp out refills it with block i + nbuf
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();  // this warp's reads of the buffer are complete
-            const int old = atomicAdd(&done[cb], 1);
-            if (old == kWarps * (i / nbuf + 1) - 1 && i + nbuf < nb) {
-                fence_proxy_async();  // generic-proxy reads -> async-proxy writes
-                issue_block(smem + cb * stage_f + kPadL * kColF,
-                            xsrc + (long)(blk0 + i + nbuf) * n * kColF, n, &full[cb]);
+
+        // ---- 4. unit epilogue: partials -> shared memory [kcnt][n_det][BB], then the
+        // fixed-rank-order cluster sum (DSMEM) -> p, and the fused MC residual for job 0
+#pragma unroll
+        for (int t = 0; t < kMaxT; ++t) {
+            const int k = tk[t];
+            if (k < 0) break;
+            const int j = tj[t];
+            if (j < n_det) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
             }
         }
-    }
-    __syncthreads();  // all blocks consumed: the buffers become the partials array
-
-    // ---- 4. partials -> shared memory [kcnt][n_det][BB], then fixed-order cluster sum
-    float *part = smem;
+        if (rank == 0 && threadIdx.x == 0) s_units[(iu + 2) & 3] = (int)atomicAdd(a.queue, 1u);
+        cluster.sync();  // partials of every rank written (cluster scope release/acquire)
+        if (rank != 0 && threadIdx.x == 0)
+            s_units[(iu + 2) & 3] = cluster.map_shared_rank(s_units, 0)[(iu + 2) & 3];
+        const float *cpart = a.scratch + (long)(blockIdx.x - rank) * part_f;  // rank 0's
+        // this rank's slice of the unit's (angle, bin) pairs; the S partials of a pair are one
+        // BB-vector each, summed in rank order
+        const int T2 = kcnt * n_det;
+        const int per2 = (T2 + S - 1) / S;
+        const int p0 = min(T2, rank * per2), p1 = min(T2, p0 + per2);
+        const long img_stride = (long)a.m * n_det;
+        const bool mc = job.y != nullptr;
+        float racc[BB];
 #pragma unroll
-    for (int t = 0; t < kMaxT; ++t) {
-        const int tau = warp + kWarps * t;
-        if (tau >= ntask) break;
-        const int k = tau / a.chunks;
-        const int j = (tau - k * a.chunks) * 32 + lane;
-        if (j < n_det) {
+        for (int b = 0; b < BB; ++b) racc[b] = 0.f;
+        for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
+            const int k = o2 / n_det;
+            const int j = o2 - k * n_det;
+            const int slot = sSlot[k];
+            float sv[BB];
+            {
+                float v[BB];
+                ldcg_vec<BB>(cpart + (long)o2 * BB, sv);
+                for (int q = 1; q < S; ++q) {
+                    ldcg_vec<BB>(cpart + q * part_f + (long)o2 * BB, v);
 #pragma unroll
-            for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
+                    for (int b = 0; b < BB; ++b) sv[b] += v[b];
+                }
+            }
+            const long pj = (long)slot * n_det + j;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
+            if (mc) {
+                const long yj = (long)idx[slot] * n_det + j;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) {
+                    const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
+                    if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
+                    racc[b] = fmaf(dr, dr, racc[b]);
+                }
+            }
+        }
+        if (mc) {  // per-(unit, rank) partial of each image of the group
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                float v = racc[b];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) s_red[warp][b] = v;
+            }
+        }
+        cluster.sync();  // partials consumed, s_units ring updated everywhere; s_red complete
+        if (mc && threadIdx.x < BB) {
+            float v = 0.f;
+            for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
+            const int slot = (u - U.uoff[d.q]) * S + rank;
+            a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + slot] = v;
         }
     }
-    cluster.sync();
-    const int T = kcnt * n_det * BB;
-    const int per = (T + S - 1) / S;
-    const int o0 = rank * per, o1 = min(T, o0 + per);
-    const long img_stride = (long)a.m * n_det;
-    for (int o = o0 + threadIdx.x; o < o1; o += kThreads) {
-        float s = 0.f;
-        for (int q = 0; q < S; ++q) s += cluster.map_shared_rank(part, q)[o];
-        const int b = o % BB;
-        const int kj = o / BB;
-        const int k = kj / n_det, j = kj - k * n_det;
-        job.p[(long)(b0 + b) * img_stride + (long)sSlot[k] * n_det + j] = s;
+
+    // ---- 5. MC residual final: the last CTA sums each image's (unit, rank) partials in order
+    if (!a.job[0].y) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.mc_ctr, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int b = warp; b < a.B; b += kWarps) {
+        const int q = b / BB;
+        const int ns = (U.uoff[q + 1] - U.uoff[q]) * S;
+        double sum = 0.0;
+        for (int i = lane; i < ns; i += 32) sum += (double)__ldcg(a.mc_part + (long)b * a.mc_slots + i);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (lane == 0) a.mc_out[b] = (float)sum;
     }
-    cluster.sync();
+    if (threadIdx.x == 0) *a.mc_ctr = 0u;  // ready for the next launch
 }
 
-// Cluster size S (line split): the number of busy units is about jobs * groups * (m/K + 1);
-// pick S in [2, 8] so that busy CTAs fill whole waves of 2 CTAs per SM.
-int pick_cluster(long units, int num_sms, int ctas_per_sm) {
-    const long slots = (long)num_sms * ctas_per_sm;
-    int best = 4;
+// Co-resident clusters of size S for this kernel configuration (cached): a persistent grid
+// must not exceed it, or the surplus clusters run as a second round.
+template <int BB>
+int max_clusters(int S, size_t smem, int num_sms) {
+    static int cache[9] = {0};
+    static size_t cache_smem[9] = {0};
+    if (cache[S] > 0 && cache_smem[S] == smem) return cache[S];
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((num_sms / S) * S), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_radon_fwd<BB>, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        ncl = num_sms / S;
+    }
+    cache[S] = ncl;
+    cache_smem[S] = smem;
+    return ncl;
+}
+
+// Cluster size S (line split) of the persistent grid: ncl(S) co-resident clusters drain a
+// queue of `units`, each costing ceil(nblk / S) + 1 blocks per CTA (the +1 is the unit's
+// prologue/epilogue); with a dynamic queue the makespan is about units / ncl rounds plus half
+// a unit of tail.  SKEI_FWD_CLUSTER=S overrides the choice (tuning/diagnostics).
+template <int BB>
+int pick_cluster(long units, int nblk, int num_sms, size_t smem, int *ncl_out) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char *e = getenv("SKEI_FWD_CLUSTER");
+        forced = e ? atoi(e) : 0;
+        if (forced < 0 || forced > 8) forced = 0;
+    }
+    int best = 4, best_ncl = 1;
     double best_cost = 1e30;
-    for (int S = 2; S <= 8; ++S) {
-        const long ctas = units * S;
-        const double waves = (double)((ctas + slots - 1) / slots);
-        const double cost = waves / S * (1.0 + 0.02 * S);  // per-CTA reduction overhead
-        if (cost < best_cost) {
+    for (int S = 1; S <= 8; ++S) {
+        const int ncl = max_clusters<BB>(S, smem, num_sms);
+        const double cost = ((double)units / ncl + 0.5) * ((nblk + S - 1) / S + 1.0);
+        if ((forced && S == forced) || (!forced && cost < best_cost - 1e-9)) {
             best_cost = cost;
             best = S;
+            best_ncl = ncl;
         }
     }
+    *ncl_out = best_ncl;
     return best;
 }
 
 template <int BB>
-cudaError_t launch_bb(FwdArgs a, int njobs, int num_sms, cudaStream_t s) {
+cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     constexpr int R = kColF / BB;
+    a.K = (kWarps * max_tasks<BB>()) / a.chunks;
+    if (a.K > kKMax) a.K = kKMax;
+    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * 32
     a.nblk = (a.g.n + R - 1) / R;
+    a.nq = a.B / BB;
+    if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
-    const size_t part_b = sizeof(float) * (size_t)a.K * a.g.n_det * BB;
-    const size_t limit = 225 * 1024;  // dynamic shared memory budget per CTA (1 CTA / SM)
+    const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~14 KB)
     a.nbuf = 3 * stage_b <= limit ? 3 : (2 * stage_b <= limit ? 2 : 1);
-    size_t smem = a.nbuf * stage_b;
-    if (part_b > smem) smem = part_b;
+    const size_t smem = a.nbuf * stage_b;
     if (smem > limit) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int ngroups = (a.m + a.K - 1) / a.K;  // per class, worst case
-    const long busy = (long)njobs * (a.B / BB) * ((a.m + a.K - 1) / a.K + 1);
-    const int S = pick_cluster(busy, num_sms, 1);
+    const long units = (long)a.njobs * a.nq * ((a.m + a.K - 1) / a.K + 1);
+    int ncl = 1;
+    const int S = pick_cluster<BB>(units, a.nblk, num_sms, smem, &ncl);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(S * 2 * ngroups), (unsigned)(a.B / BB), (unsigned)njobs);
+    cfg.gridDim = dim3((unsigned)(ncl * S), 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -394,25 +635,46 @@ cudaError_t launch_bb(FwdArgs a, int njobs, int num_sms, cudaStream_t s) {
 
 }  // namespace
 
+size_t fwd_scratch_floats(const skei_plan *plan) {
+    // grid <= num_sms CTAs, each K * n_det * BB <= kWarps * kMaxT * 32 * 4 floats
+    return (size_t)plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
+}
+
+size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
+    (void)B;
+    (void)idx_stride;
+    const int chunks = (plan->n_det + 31) / 32;
+    int K = (kWarps * max_tasks<1>()) / chunks;  // the smallest K over the image groups
+    if (K > kKMax) K = kKMax;
+    if (K < 1) K = 1;
+    return (size_t)8 * ((m + K - 1) / K + 2);  // cluster size x units per image group
+}
+
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
-                             const int32_t *idx, int m, int idx_stride, cudaStream_t s) {
+                             const int32_t *idx, int m, int idx_stride, const FwdScratch &scr,
+                             cudaStream_t s, const FwdMc *mc) {
     FwdArgs a;
+    a.queue = scr.queue;
+    a.scratch = scr.part;
+    a.mc_part = mc ? mc->part : nullptr;
+    a.mc_slots = (int)fwd_mc_slots(plan, B, m, idx_stride);
+    a.mc_ctr = mc ? mc->ctr : nullptr;
+    a.mc_out = mc ? mc->out : nullptr;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
+    a.njobs = njobs;
     a.idx = idx;
     a.m = m;
     a.idx_stride = idx_stride;
     a.B = B;
     a.g = geom_of(plan);
     a.chunks = (plan->n_det + 31) / 32;
-    a.K = (kWarps * kMaxT) / a.chunks;
-    if (a.K > kKMax) a.K = kKMax;
-    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * 32
-    const int bb = pick_bb(B, idx_stride);
+    if (!mc) a.job[0].y = nullptr;
+    const int bb = fwd_bb(B, idx_stride);
     switch (bb) {
-        case 4: return launch_bb<4>(a, njobs, plan->num_sms, s);
-        case 2: return launch_bb<2>(a, njobs, plan->num_sms, s);
-        default: return launch_bb<1>(a, njobs, plan->num_sms, s);
+        case 4: return launch_bb<4>(a, plan->num_sms, s);
+        case 2: return launch_bb<2>(a, plan->num_sms, s);
+        default: return launch_bb<1>(a, plan->num_sms, s);
     }
 }
 

@@ -5,7 +5,7 @@
 // k_rotate_pack: one CTA = an 8 x 32 pixel tile of BB images that share g (BB = the image
 // group of the forward projector).  Each thread forms the fp64 source coordinates of one
 // output pixel once and applies them to its BB images (4 taps each, read-only path).  It
-// writes, as requested:
+// writes, as requested (cos g, sin g come from the plan's fp64 table of the 360 angles):
 //   * the plain rotated image out[b][r][c]                          (skei_rotate's output)
 //   * the row-packed copy  xr[grp][r / R][c][r % R][b]  (R = 32 / BB lines per block)
 //   * the col-packed copy  xc[grp][c / R][r][c % R][b]
@@ -20,19 +20,11 @@ namespace {
 
 constexpr int kTR = 8, kTC = 32;  // tile rows x columns
 
-__device__ inline void cossin_deg(int g, double *c, double *s) {
-    int gm = ((g % 360) + 360) % 360;
-    if (gm == 0) { *c = 1.0; *s = 0.0; return; }
-    if (gm == 90) { *c = 0.0; *s = 1.0; return; }
-    if (gm == 180) { *c = -1.0; *s = 0.0; return; }
-    if (gm == 270) { *c = 0.0; *s = -1.0; return; }
-    sincospi((double)gm / 180.0, s, c);
-}
-
 template <int BB>
 __global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
     constexpr int R = 32 / BB;
-    __shared__ float tile[kTR][kTC][BB];
+    constexpr int kRow = kTC * BB + 4;  // padded tile row (floats): conflict-free pack reads
+    __shared__ __align__(16) float tile[kTR * kRow];
     const RotPackJob job = blockIdx.z ? a.job[1] : a.job[0];
     const int n = a.n;
     const int tr = threadIdx.x / kTC, tc = threadIdx.x % kTC;
@@ -41,6 +33,9 @@ __global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
     const int b0 = blockIdx.y * BB;
     const long nn = (long)n * n;
     const bool inside = r < n && c < n;
+    if (job.zero && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+        job.zero[0] = job.zero[1] = job.zero[2] = 0u;  // the pass's counters (fused
+                                                        // reductions, forward work queue)
 
     float v[BB];
 #pragma unroll
@@ -65,8 +60,9 @@ __global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
                 const int gd = job.g[job.g_stride ? b0 + b : 0];
                 if (gd != gprev) {
                     gprev = gd;
-                    double cg, sg;
-                    cossin_deg(gd, &cg, &sg);
+                    // (cos g, sin g) from the plan's fp64 table (exact at multiples of 90)
+                    const double2 csg = a.rot[((gd % 360) + 360) % 360];
+                    const double cg = csg.x, sg = csg.y;
                     const double us = u * cg + w * sg;
                     const double vs = -u * sg + w * cg;
                     const double cs = us + h, rs = h - vs;
@@ -99,18 +95,28 @@ __global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
         }
     }
     if (!job.xr && !job.xc) return;
+    {
+        float *tp = tile + tr * kRow + tc * BB;
+        if constexpr (BB == 4) {
+            *reinterpret_cast<float4 *>(tp) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
 #pragma unroll
-    for (int b = 0; b < BB; ++b) tile[tr][tc][b] = v[b];
+            for (int b = 0; b < BB; ++b) tp[b] = v[b];
+        }
+    }
     __syncthreads();
     const long grp_stride = (long)a.nblk * n * 32;  // floats per image group per class
     const int e = threadIdx.x;                    // 256 threads, one float each per pass
     if (job.xr) {
-        // row-packed: for each tile column c, lines r0..r0+7 of block r0/R are contiguous
-        // (8 x BB floats at offset (r0 % R) * BB): 32 columns x (8*BB) floats
-        float *dst = job.xr + blockIdx.y * grp_stride + ((long)(r0 / R) * n) * 32 + (r0 % R) * BB;
+        // row-packed: for each tile column c, the tile's rows are consecutive line slots of
+        // their block (R >= 8: one block, 8 x BB contiguous floats)
+        float *dst = job.xr + blockIdx.y * grp_stride;
         for (int q = e; q < kTC * kTR * BB; q += kTR * kTC) {
             const int b = q % BB, l = (q / BB) % kTR, cc = q / (BB * kTR);
-            if (c0 + cc < n) dst[(long)(c0 + cc) * 32 + l * BB + b] = tile[l][cc][b];
+            const int row = r0 + l;
+            if (c0 + cc < n)
+                dst[((long)(row / R) * n + c0 + cc) * 32 + (row % R) * BB + b] =
+                    tile[l * kRow + cc * BB + b];
         }
     }
     if (job.xc) {
@@ -120,7 +126,7 @@ __global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
         for (int q = e; q < kTR * kTC * BB; q += kTR * kTC) {
             const int b = q % BB, cc = (q / BB) % kTC, l = q / (BB * kTC);
             const int col = c0 + cc, row = r0 + l;
-            if (row < n && col < a.nblk * R) dst[((long)(col / R) * n + row) * 32 + (col % R) * BB + b] = tile[l][cc][b];
+            if (row < n && col < a.nblk * R) dst[((long)(col / R) * n + row) * 32 + (col % R) * BB + b] = tile[l * kRow + cc * BB + b];
         }
     }
 }
@@ -140,6 +146,7 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
     a.n = plan->n;
     a.B = B;
+    a.rot = plan->d_rot;
     const int R = 32 / bb;
     a.nblk = (plan->n + R - 1) / R;
     a.tiles_c = (plan->n + kTC - 1) / kTC;
@@ -157,7 +164,7 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
 
 cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
                           const int32_t *g, int g_stride, cudaStream_t s) {
-    RotPackJob j{x, out, g, g_stride, nullptr, nullptr};
+    RotPackJob j{x, out, g, g_stride, nullptr, nullptr, nullptr};
     const int bb = B % 4 == 0 ? 4 : (B % 2 == 0 ? 2 : 1);
     return launch_rotate_pack(plan, &j, 1, B, bb, s);
 }

@@ -16,7 +16,20 @@ def main():
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[1]
+    kre = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else None
+    # the page holds one section per kernel: ["Kernel Name", name], header, rows...
+    secs, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = [r[1] if len(r) > 1 else "", None, []]
+            secs.append(cur)
+        elif cur is not None and cur[1] is None:
+            cur[1] = r
+        elif cur is not None:
+            cur[2].append(r)
+    sec = next(s for s in secs if kre is None or re.search(kre, s[0]))
+    print("kernel:", sec[0][:100])
+    hdr, rows = sec[1], [None, None] + sec[2]
     isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
     iss = hdr.index("Warp Stall Sampling (All Samples)")
     iwf = hdr.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in hdr else None
