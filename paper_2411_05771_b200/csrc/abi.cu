@@ -124,7 +124,8 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
         P = 2;
         while (P < 2 * n_det - 1) P *= 2;
     }
-    if (!is_pow2(P) || P < 2 * n_det - 1 || P > 16384 || P < 4) return SKEI_ERR_CONFIG;
+    if (P < 16 && geom->fft_len == 0) P = 16;  // the FFT kernel needs P >= 16
+    if (!is_pow2(P) || P < 2 * n_det - 1 || P > 8192 || P < 16) return SKEI_ERR_CONFIG;
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
@@ -169,11 +170,17 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
         else if (g == 270) rot[g] = make_double2(0.0, -1.0);
         else rot[g] = make_double2(std::cos(M_PI * g / 180.0), std::sin(M_PI * g / 180.0));
     }
-    std::vector<float2> tw(P / 2);
-    for (int k = 0; k < P / 2; ++k) {
-        double a = 2.0 * M_PI * (double)k / (double)P;
-        tw[k] = make_float2((float)std::cos(a), (float)(-std::sin(a)));
-    }
+    int npass = 0, radix[kMaxFftPass], ns[kMaxFftPass], twoff[kMaxFftPass], twtotal = 0;
+    fft_plan(P, &npass, radix, ns, twoff, &twtotal);
+    std::vector<float2> tw(twtotal);
+    for (int ip = 0; ip < npass; ++ip)
+        for (int k = 0; k < ns[ip]; ++k)
+            for (int r = 0; r < radix[ip]; ++r) {
+                // exp(-2 pi i r k / (R Ns)), reduced exactly before the fp64 trig
+                const long num = ((long)r * k) % ((long)radix[ip] * ns[ip]);
+                const double a = 2.0 * M_PI * (double)num / ((double)radix[ip] * ns[ip]);
+                tw[twoff[ip] + k * radix[ip] + r] = make_float2((float)std::cos(a), (float)(-std::sin(a)));
+            }
 
     skei_plan *p = new skei_plan();
     p->device = device;
@@ -186,7 +193,13 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     p->num_sms = prop.multiProcessorCount;
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * n_full);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_ramp, sizeof(float) * P);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_tw, sizeof(float2) * (P / 2));
+    p->fft_npass = npass;
+    for (int i = 0; i < npass; ++i) {
+        p->fft_radix[i] = radix[i];
+        p->fft_ns[i] = ns[i];
+        p->fft_twoff[i] = twoff[i];
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_twp, sizeof(float2) * twtotal);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_rot, sizeof(double2) * 360);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_rot, rot.data(), sizeof(double2) * 360, cudaMemcpyHostToDevice);
@@ -195,7 +208,7 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_ramp, ramp.data(), sizeof(float) * P, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
-        e = cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * (P / 2), cudaMemcpyHostToDevice);
+        e = cudaMemcpy(p->d_twp, tw.data(), sizeof(float2) * twtotal, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         skei_plan_destroy(p);
         return cuda_fail(e);
@@ -209,7 +222,7 @@ void skei_plan_destroy(skei_plan *plan) {
     DeviceGuard guard(plan->device);
     if (plan->d_trig) cudaFree(plan->d_trig);
     if (plan->d_ramp) cudaFree(plan->d_ramp);
-    if (plan->d_tw) cudaFree(plan->d_tw);
+    if (plan->d_twp) cudaFree(plan->d_twp);
     if (plan->d_rot) cudaFree(plan->d_rot);
     delete plan;
 }

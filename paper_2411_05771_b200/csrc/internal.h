@@ -7,13 +7,18 @@
 
 #include "../../include/skei.h"
 
+constexpr int kMaxFftPass = 8;
+
 struct skei_plan {
     int device;
     int n, n_det, n_full, fft_len, log2_fft;
     int num_sms;
     double2 *d_trig;  // [n_full] (cos, sin) of theta_i = i*pi/n_full, fp64
     float *d_ramp;    // [fft_len] R[k] / P, fp32 (from an fp64 DFT)
-    float2 *d_tw;     // [fft_len/2] exp(-2 pi i k / P), fp32 (from fp64)
+    // FFT pass plan (ramp.cu): radix, sub-transform length Ns and twiddle-table offset per
+    // pass; d_twp[off + k R + r] = exp(-2 pi i r k / (R Ns)), fp32 rounded from fp64
+    int fft_npass, fft_radix[kMaxFftPass], fft_ns[kMaxFftPass], fft_twoff[kMaxFftPass];
+    float2 *d_twp;
     double2 *d_rot;   // [360] (cos g, sin g) of g degrees, fp64, exact at multiples of 90
 };
 
@@ -98,6 +103,7 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
                              const AdjEi *ei = nullptr);
 
+void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s);
 

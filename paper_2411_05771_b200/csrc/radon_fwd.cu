@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ __align__(8) uint64_t full[3];
     __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
-    __shared__ float sAbsB[kKMax], sSec[kKMax], sPlf[kKMax];
+    __shared__ float sAbsB[kKMax];
+    __shared__ float4 sAng[kKMax];  // |beta|, 1/|beta|, Pl, 2 - 3|beta| (fp32)
     __shared__ int sSlot[kKMax];
     __shared__ int sCount;
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     const int K = a.K, nq = a.nq;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int stage_f = (n + kPadL + kPadR) * kColF;
+    int4 *btab = reinterpret_cast<int4 *>(smem + a.nbuf * stage_f);  // [K][nb] block table
     const long part_f = (long)K * n_det * BB;
     float *part = a.scratch + (long)blockIdx.x * part_f;  // this CTA's partials (L2)
 
@@ -308,7 +310,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     }
     const unsigned smem_b = smem_u32(smem);
     const unsigned cmax = (unsigned)(n + 3);
-    const float fn1 = (float)(n - 1);
 
     for (int iu = 0;; ++iu) {
         const int u = s_units[iu & 3];
@@ -355,22 +356,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 sPj[lane] = Pj;
                 sPl[lane] = Pl;
                 sAbsB[lane] = (float)ab;
-                sSec[lane] = (float)(1.0 / ab);
-                sPlf[lane] = (float)Pl;
+                sAng[lane] = make_float4((float)ab, (float)(1.0 / ab), (float)Pl,
+                                         (float)(2.0 - 3.0 * ab));
             }
         }
         __syncthreads();
         const int kcnt = sCount;
         const int ntask = kcnt * a.chunks;
+        // per (angle, block): the block's first-line position of bin 0, A = P0 + lb Pl, split
+        // into (int base, fp32 frac) in fp64, and the exact range [jlo, jhi] of bins whose
+        // candidates can fall inside the image for some line of the block
+        for (int e = threadIdx.x; e < kcnt * nb; e += kThreads) {
+            const int k = e / nb, i = e - k * nb;
+            const double Pl = sPl[k], Pj = sPj[k];
+            const double A = sP0[k] + (double)((blk0 + i) * R) * Pl;
+            const double fA = floor(A);
+            const double sec = 1.0 / (double)sAbsB[k];
+            const double lmin = fmin(0.0, (R - 1) * Pl), lmax = fmax(0.0, (R - 1) * Pl);
+            // bin j touches the block iff A + j Pj + [lmin, lmax] meets (-sec - 1, n - 1 + sec + 1)
+            const double u0 = (-sec - 1.0 - A - lmax) / Pj, u1 = (n - 1 + sec + 1.0 - A - lmin) / Pj;
+            const double jl = fmax(-1.0, floor(fmin(u0, u1))), jh = fmin((double)n_det, ceil(fmax(u0, u1)));
+            int4 ent;
+            ent.x = (int)fA;
+            ent.y = __float_as_int((float)(A - fA));
+            ent.z = (int)jl;
+            ent.w = (int)jh;
+            btab[e] = ent;
+        }
 
         // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps
-        int tk[kMaxT], tj[kMaxT];  // angle slot and bin of this lane's tasks (tk < 0: none)
+        // per task: angle slot tk (< 0: none), first bin of the chunk tc, and j Pj split into
+        // (int jb, fp32 jf) in fp64 (the bin-dependent part of the position)
+        int tk[kMaxT], tc[kMaxT], jb[kMaxT];
+        float jf[kMaxT];
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t) {
             const int tau = warp + kWarps * t;
             tk[t] = tau < ntask ? tau / a.chunks : -1;
-            tj[t] = tau < ntask ? (tau - tk[t] * a.chunks) * 32 + lane : 0;
+            tc[t] = tau < ntask ? (tau - tk[t] * a.chunks) * 32 : 0;
+            const double J = (double)(tc[t] + lane) * sPj[tk[t] < 0 ? 0 : tk[t]];
+            const double fJ = floor(J);
+            jb[t] = (int)fJ;
+            jf[t] = (float)(J - fJ);
         }
+        __syncthreads();  // block table complete
         float acc[kMaxT][BB];
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t)
@@ -387,31 +416,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             for (int t = 0; t < kMaxT; ++t) {
                 const int k = tk[t];
                 if (k < 0) break;  // warp-uniform
-                const int j = tj[t];
-                const double Pl = sPl[k];
-                const double ad = sP0[k] + (double)lb * Pl + (double)j * sPj[k];
-                const double fl = floor(ad);
-                const int base = (int)fl;
-                const float frac = (float)(ad - fl);
-                const float ab = sAbsB[k], sec = sSec[k], plf = sPlf[k];
-                // does any bin of this chunk see a line of this block?
-                const float span = (float)(R - 1) * plf;
-                const float lo = (float)base + frac + fminf(0.f, span);
-                const float hi = (float)base + frac + fmaxf(0.f, span);
-                const bool act = j < n_det && hi + sec > 0.f && lo - sec < fn1;
-                if (!__any_sync(0xffffffffu, act)) continue;
-                const float c1 = 2.f * ab - 1.f, c2 = 2.f - 3.f * ab;
-                const float fs = frac - sec;
+                const int4 ent = btab[k * nb + i];
+                if (tc[t] > ent.w || tc[t] + 31 < ent.z) continue;  // chunk misses the block
+                int base = ent.x + jb[t];
+                float frac = __int_as_float(ent.y) + jf[t];
+                if (frac >= 1.f) {
+                    frac -= 1.f;
+                    base += 1;
+                }
+                const float4 ang = sAng[k];  // |beta|, 1/|beta|, Pl, 2 - 3|beta|
+                const float ab = ang.x, plf = ang.z, c2 = ang.w;
+                const float c1 = fmaf(2.f, ab, -1.f);
+                const float fs = frac - ang.y;
                 const int base4 = base + 4;
                 float blk[BB];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) blk[b] = 0.f;
 #pragma unroll
-                for (int s = 0; s < R; ++s) {
+                for (int st = 0; st < R; ++st) {
                     // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
                     // phi = e - floor(e) the hat weights of the 3 candidates are
                     //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
-                    const float e = fmaf(lfs[s], plf, fs);
+                    const float e = fmaf(lfs[st], plf, fs);
                     const float fl2 = floorf(e);
                     const float phi = e - fl2;
                     // candidate_0 + 3 clamped to [0, n + 3] in one unsigned min (lanes whose
@@ -420,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     const float w0 = fmaf(-ab, phi, ab);
                     const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
                     const float w2 = fmaf(ab, phi, c2);
-                    const unsigned pa = cur_b + cu * (unsigned)(kColF * sizeof(float)) + lofs[s];
+                    const unsigned pa = cur_b + cu * (unsigned)(kColF * sizeof(float)) + lofs[st];
                     float v0[BB], v1[BB], v2[BB];
                     lds_px<BB>(pa, v0);
                     lds_px<BB>(pa + kColF * sizeof(float), v1);
@@ -455,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         for (int t = 0; t < kMaxT; ++t) {
             const int k = tk[t];
             if (k < 0) break;
-            const int j = tj[t];
+            const int j = tc[t] + lane;
             if (j < n_det) {
 #pragma unroll
                 for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
@@ -606,9 +632,10 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     a.nq = a.B / BB;
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
+    const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
     const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~14 KB)
-    a.nbuf = 3 * stage_b <= limit ? 3 : (2 * stage_b <= limit ? 2 : 1);
-    const size_t smem = a.nbuf * stage_b;
+    a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
+    const size_t smem = a.nbuf * stage_b + tab_b;
     if (smem > limit) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -2,129 +2,233 @@
 // north_star's "batched zero-padded real FFT-multiply kernel".
 //
 // Two real rows are packed into one complex sequence z = p_a + i p_b, zero-padded to
-// P >= 2 n_det - 1 (so the circular convolution equals the linear one on the first
-// n_det outputs).  Because the spectrum R[k] is real and even,
-// IFFT(R . FFT(z)) = (h2 (*) p_a) + i (h2 (*) p_b): no post-processing twiddles.  The
-// FFT is an in-shared-memory Stockham autosort transform, radix-4 stages plus one
-// radix-2 stage when log2 P is odd; twiddles and R come from fp64-derived plan tables.
+// P >= 2 n_det - 1 (so the circular convolution equals the linear one on the first n_det
+// outputs).  Because the spectrum R[k] is real and even,
+// IFFT(R . FFT(z)) = (h2 (*) p_a) + i (h2 (*) p_b): no un-packing twiddles.
+//
+// The FFT is a Stockham autosort transform of radix-16 passes plus one final pass of the
+// remaining factor (8, 4 or 2); each thread holds 16 complex values (one radix-16
+// butterfly, or 16/R radix-R butterflies) in registers:
+//   pass (R, Ns): for j < P/R, k = j mod Ns: v_r = z[j + r P/R] w^(r k), w = e^(-2 pi i /
+//   (R Ns)); y = DFT_R(v); z'[(j - k) R + k + q Ns] = y_q.
+// One CTA = one packed pair of rows, P/16 threads.  Passes exchange through one padded
+// shared-memory buffer in place (element e at e + e/16: conflict-free for the strides of
+// every pass); the first pass reads the rows straight from global memory, the spectrum is
+// multiplied by R[k]/P as the inverse transform loads it, and the last inverse pass writes
+// the two output rows straight to global memory.  Twiddles w^(rk) come from per-pass plan
+// tables computed in fp64 and rounded once (no recurrences, no fast intrinsics); the
+// in-register DFT uses the exact 16th roots of unity as literals.
 #include "internal.h"
 
 namespace skei {
 namespace {
 
-constexpr int kThreads = 256;
-
-__device__ inline float2 cmul(float2 a, float2 b) {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-__device__ inline float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ inline float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-// multiply by -i (forward) or +i (inverse)
-__device__ inline float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
-__device__ inline float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }
-
-// twiddle exp(-+2 pi i e / P) for 0 <= e < P from the half table tw[0, P/2)
-__device__ inline float2 twiddle(const float2 *tw, int e, int half, bool inverse) {
-    float2 w = e < half ? tw[e] : make_float2(-tw[e - half].x, -tw[e - half].y);
-    if (inverse) w.y = -w.y;
-    return w;
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
+__device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
-// One full complex FFT of length P = 2^logP in shared memory; returns the buffer that
-// holds the result.
-__device__ float2 *stockham(float2 *a, float2 *b, const float2 *tw, int P, int logP,
-                            bool inverse) {
-    const int half = P / 2;
-    int Ns = 1;
-    int s = 0;
-    for (; s + 2 <= logP; s += 2) {  // radix-4 stages
-        const int quarter = P / 4;
-        const int tstep = P / (4 * Ns);
-        for (int j = threadIdx.x; j < quarter; j += blockDim.x) {
-            const int k = j & (Ns - 1);
-            float2 v0 = a[j], v1 = a[j + quarter], v2 = a[j + 2 * quarter], v3 = a[j + 3 * quarter];
-            if (Ns > 1) {
-                v1 = cmul(v1, twiddle(tw, k * tstep, half, inverse));
-                v2 = cmul(v2, twiddle(tw, 2 * k * tstep, half, inverse));
-                v3 = cmul(v3, twiddle(tw, 3 * k * tstep, half, inverse));
+// cos / sin of 2 pi t / 16, t = 0..7
+__device__ __constant__ float kC16[8] = {1.0f, 0.92387953251128674f, 0.70710678118654757f,
+                                         0.38268343236508978f, 0.0f, -0.38268343236508978f,
+                                         -0.70710678118654757f, -0.92387953251128674f};
+__device__ __constant__ float kS16[8] = {0.0f, 0.38268343236508978f, 0.70710678118654757f,
+                                         0.92387953251128674f, 1.0f, 0.92387953251128674f,
+                                         0.70710678118654757f, 0.38268343236508978f};
+
+// In-register DFT of size R: y_q = sum_r v_r exp(-+2 pi i q r / R) (iterative radix-2,
+// bit-reversed inputs, natural-order outputs).
+template <int R>
+__device__ __forceinline__ void dft(float2 (&v)[R], bool inverse) {
+    constexpr int L = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        int r = 0;
+#pragma unroll
+        for (int b = 0; b < L; ++b) r |= ((i >> b) & 1) << (L - 1 - b);
+        if (r > i) {
+            const float2 t = v[i];
+            v[i] = v[r];
+            v[r] = t;
+        }
+    }
+#pragma unroll
+    for (int s = 1; s <= L; ++s) {
+        const int m = 1 << s, h = m >> 1;
+#pragma unroll
+        for (int jj = 0; jj < h; ++jj) {
+            const int t = jj * (16 / m);  // angle 2 pi t / 16
+            const float wr = kC16[t];
+            const float wi = inverse ? kS16[t] : -kS16[t];
+#pragma unroll
+            for (int k = 0; k < R; k += m) {
+                const float2 a = v[k + jj], b = v[k + jj + h];
+                float2 tb;
+                if (jj == 0) {
+                    tb = b;
+                } else if (4 * jj == m) {  // w = -+i
+                    tb = inverse ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
+                } else {
+                    tb = make_float2(fmaf(b.x, wr, -b.y * wi), fmaf(b.x, wi, b.y * wr));
+                }
+                v[k + jj] = make_float2(a.x + tb.x, a.y + tb.y);
+                v[k + jj + h] = make_float2(a.x - tb.x, a.y - tb.y);
             }
-            const float2 s02 = cadd(v0, v2), d02 = csub(v0, v2);
-            const float2 s13 = cadd(v1, v3), d13 = csub(v1, v3);
-            const float2 r13 = inverse ? mul_pi(d13) : mul_mi(d13);
-            const int d = (j - k) * 4 + k;
-            b[d] = cadd(s02, s13);
-            b[d + Ns] = cadd(d02, r13);
-            b[d + 2 * Ns] = csub(s02, s13);
-            b[d + 3 * Ns] = csub(d02, r13);
         }
-        __syncthreads();
-        float2 *t = a;
-        a = b;
-        b = t;
-        Ns *= 4;
     }
-    if (s < logP) {  // final radix-2 stage
-        const int tstep = P / (2 * Ns);
-        for (int j = threadIdx.x; j < half; j += blockDim.x) {
-            const int k = j & (Ns - 1);
-            const float2 v0 = a[j];
-            const float2 v1 = cmul(a[j + half], twiddle(tw, k * tstep, half, inverse));
-            const int d = (j - k) * 2 + k;
-            b[d] = cadd(v0, v1);
-            b[d + Ns] = csub(v0, v1);
-        }
-        __syncthreads();
-        a = b;
-    }
-    return a;
 }
 
-__global__ void __launch_bounds__(kThreads) k_ramp(const float *__restrict__ p, float *q,
-                                                   int rows, int n_det, int P, int logP,
-                                                   const float2 *__restrict__ tw_g,
-                                                   const float *__restrict__ R) {
-    extern __shared__ float2 sm[];
-    float2 *bufA = sm, *bufB = sm + P, *tw = sm + 2 * P;  // tw: [P/2]
-    const int ra = 2 * blockIdx.x, rb = ra + 1;
-    const bool has_b = rb < rows;
-    for (int i = threadIdx.x; i < P / 2; i += blockDim.x) tw[i] = tw_g[i];
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        float xa = 0.f, xb = 0.f;
-        if (i < n_det) {
-            xa = p[(long)ra * n_det + i];
-            if (has_b) xb = p[(long)rb * n_det + i];
+struct RampArgs {
+    const float *p;
+    float *q;
+    int rows, n_det, P;
+    const float *R;    // [P] spectrum / P
+    const float2 *tw;  // per-pass twiddle tables [k][r], k < Ns, r < R
+    int npass;
+};
+
+// One Stockham pass (in place on z): J = 16/R butterflies per thread.  mode flags:
+// kIn = read the two input rows from global (first forward pass), kScale = multiply by
+// R[i] as loaded (first inverse pass), kOut = write the two output rows to global (last
+// inverse pass); otherwise smem -> smem.
+constexpr int kIn = 1, kScale = 2, kOut = 4;
+template <int R>
+__device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool inverse, int mode,
+                                     const float *pa, const float *pb, float *qa, float *qb) {
+    constexpr int J = 16 / R;
+    // every pass before `ip` is radix 16: Ns = 16^ip, table offset = sum_{i<ip} 16 * 16^i
+    const int Ns = 1 << (4 * ip), stride = a.P / R;
+    const float2 *tw = a.tw + 16 * (Ns - 1) / 15;
+    float2 v[J][R];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        const int j = threadIdx.x + jj * blockDim.x;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = j + r * stride;
+            if (mode & kIn) {
+                v[jj][r] = i < a.n_det ? make_float2(__ldg(pa + i), pb ? __ldg(pb + i) : 0.f)
+                                       : make_float2(0.f, 0.f);
+            } else {
+                v[jj][r] = z[pad(i)];
+                if (mode & kScale) {
+                    const float s = __ldg(a.R + i);
+                    v[jj][r].x *= s;
+                    v[jj][r].y *= s;
+                }
+            }
         }
-        bufA[i] = make_float2(xa, xb);
     }
-    __syncthreads();
-    float2 *z = stockham(bufA, bufB, tw, P, logP, false);
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const float r = R[i];
-        z[i] = make_float2(z[i].x * r, z[i].y * r);
+    if (!(mode & kIn)) __syncthreads();  // every read of this pass precedes every write
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        const int j = threadIdx.x + jj * blockDim.x;
+        const int k = j & (Ns - 1);
+        if (Ns > 1) {
+            const float2 *t = tw + (long)k * R;
+#pragma unroll
+            for (int r = 1; r < R; ++r)
+                v[jj][r] = inverse ? cmulc(v[jj][r], __ldg(t + r)) : cmul(v[jj][r], __ldg(t + r));
+        }
+        dft<R>(v[jj], inverse);
+        const int d = (j - k) * R + k;
+        if (mode & kOut) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int o = d + q * Ns;
+                if (o < a.n_det) {
+                    qa[o] = v[jj][q].x;
+                    if (qb) qb[o] = v[jj][q].y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < R; ++q) z[pad(d + q * Ns)] = v[jj][q];
+        }
     }
-    __syncthreads();
-    float2 *other = (z == bufA) ? bufB : bufA;
-    z = stockham(z, other, tw, P, logP, true);
-    for (int i = threadIdx.x; i < n_det; i += blockDim.x) {
-        q[(long)ra * n_det + i] = z[i].x;
-        if (has_b) q[(long)rb * n_det + i] = z[i].y;
-    }
+    if (!(mode & kOut)) __syncthreads();
+}
+
+template <int RL>
+__global__ void __launch_bounds__(512) k_ramp(RampArgs a) {  // P/16 <= 512 threads
+    extern __shared__ float2 z[];
+    const int ra = 2 * blockIdx.x, rb = ra + 1;
+    const bool has_b = rb < a.rows;
+    const float *pa = a.p + (long)ra * a.n_det;
+    const float *pb = has_b ? a.p + (long)rb * a.n_det : nullptr;
+    float *qa = a.q + (long)ra * a.n_det;
+    float *qb = has_b ? a.q + (long)rb * a.n_det : nullptr;
+    const int last = a.npass - 1;
+    // forward: radix-16 passes then the RL pass
+    for (int ip = 0; ip < last; ++ip) pass<16>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb);
+    pass<RL>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb);
+    // inverse of R . FFT(z)
+    for (int ip = 0; ip < last; ++ip)
+        pass<16>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb);
+    pass<RL>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb);
 }
 
 }  // namespace
 
+// Pass plan of a P-point transform (P a power of two >= 16): radix-16 passes, then one
+// pass of the remaining factor 8, 4 or 2.  Twiddle table offsets are in complex entries.
+void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal) {
+    int n = 0, Ns = 1, off = 0;
+    int rem = P;
+    while (rem >= 16) {
+        radix[n] = 16;
+        ns[n] = Ns;
+        twoff[n] = off;
+        off += 16 * Ns;
+        Ns *= 16;
+        rem /= 16;
+        ++n;
+    }
+    if (rem > 1) {  // final pass of 8, 4 or 2
+        radix[n] = rem;
+        ns[n] = Ns;
+        twoff[n] = off;
+        off += rem * Ns;
+        ++n;
+    }
+    *npass = n;
+    *twtotal = off;
+}
+
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s) {
-    const int P = plan->fft_len;
-    const size_t smem = sizeof(float2) * (2 * (size_t)P + P / 2);
-    if (smem > 48 * 1024) {  // per-device attribute: set on every call (cheap)
-        cudaError_t e =
-            cudaFuncSetAttribute(k_ramp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
+    RampArgs a;
+    a.p = p;
+    a.q = q;
+    a.rows = rows;
+    a.n_det = plan->n_det;
+    a.P = plan->fft_len;
+    a.R = plan->d_ramp;
+    a.tw = plan->d_twp;
+    a.npass = plan->fft_npass;
+    const int RL = plan->fft_radix[plan->fft_npass - 1];
+    const size_t smem = sizeof(float2) * (size_t)(a.P + a.P / 16);
+    const int threads = a.P / 16;
     const int grid = (rows + 1) / 2;
-    k_ramp<<<grid, kThreads, smem, s>>>(p, q, rows, plan->n_det, P, plan->log2_fft, plan->d_tw,
-                                        plan->d_ramp);
+    cudaError_t e = cudaSuccess;
+#define SKEI_RAMP_LAUNCH(RLV)                                                                   \
+    do {                                                                                        \
+        if (smem > 48 * 1024)                                                                   \
+            e = cudaFuncSetAttribute(k_ramp<RLV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                     (int)smem);                                                \
+        if (e == cudaSuccess) k_ramp<RLV><<<grid, threads, smem, s>>>(a);                      \
+    } while (0)
+    switch (RL) {
+        case 16: SKEI_RAMP_LAUNCH(16); break;
+        case 8: SKEI_RAMP_LAUNCH(8); break;
+        case 4: SKEI_RAMP_LAUNCH(4); break;
+        default: SKEI_RAMP_LAUNCH(2); break;
+    }
+#undef SKEI_RAMP_LAUNCH
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
