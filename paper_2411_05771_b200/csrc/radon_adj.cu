@@ -28,7 +28,8 @@ namespace skei {
 namespace {
 
 constexpr int kTile = 32;      // tile side (pixels)
-constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 16 columns
+constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 16 columns (8 pixel pairs)
+constexpr int kPairs = 2;      // pixel pairs per thread
 constexpr int kKC = 12;        // angles per staged chunk (2 buffers x 2 jobs fit 48 KB)
 constexpr int kW = 48;         // staged bins per angle (>= 31 sqrt 2 + 3)
 
@@ -89,17 +90,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
     const int b0 = blockIdx.y * BB;
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // warp w: rows 8*(w/2) .. +7, columns 16*(w%2) .. +15; lane: row (lane % 8), pair
-    // columns (lane / 8) and (lane / 8) + 4 of the warp's 8 pairs
+    // warp w: rows 8*(w/2) .. +7, pixel pairs 8*(w%2) .. +7; lane: row (lane % 8), pairs
+    // (lane / 8) and (lane / 8) + 4 — the 8 lanes of a quarter-warp are 8 consecutive rows
+    // of one pair
     const int ry = 8 * (warp >> 1) + (lane & 7);
     const int pc0 = 8 * (warp & 1) + (lane >> 3);  // pair index 0..15, second pair = +4
     const long nn = (long)n * n;
 
-    float acc[NJ][2][2][BB];  // [job][pair][pixel][image]
+    float acc[NJ][kPairs][2][BB];  // [job][pair][pixel][image]
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+        for (int p = 0; p < kPairs; ++p)
 #pragma unroll
             for (int q = 0; q < 2; ++q)
 #pragma unroll
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             // position of pixel (ry, 2 pc) relative to the window origin
             const float rowb = fmaf(-(float)ry, st, s_off[bf][t]);
 #pragma unroll
-            for (int p = 0; p < 2; ++p) {
+            for (int p = 0; p < kPairs; ++p) {
                 const int c = 2 * (pc0 + 4 * p);
                 const float t1 = fmaf((float)c, ct, rowb);
                 const float t2 = t1 + ct;
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
     for (int jj = 0; jj < NJ; ++jj) {
         const float sc = a.job[jj].scale;
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
+        for (int p = 0; p < kPairs; ++p) {
             const int c = tc0 + 2 * (pc0 + 4 * p);
             if (r >= n) continue;
 #pragma unroll

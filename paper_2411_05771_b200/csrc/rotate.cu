@@ -2,10 +2,11 @@
 // zero outside, about the image centre, counter-clockwise for g > 0 (R11), fused
 // with the packing of the forward projector's input.
 //
-// k_rotate_pack: one CTA = an 8 x 32 pixel tile of BB images that share g (BB = the image
-// group of the forward projector).  Each thread forms the fp64 source coordinates of one
-// output pixel once and applies them to its BB images (4 taps each, read-only path).  It
-// writes, as requested (cos g, sin g come from the plan's fp64 table of the 360 angles):
+// k_rotate_pack: one CTA = a 32 x 32 pixel tile of BB images (BB = the image group of the
+// forward projector), a thread per column and 4 rows.  Source coordinates in split precision: the tile origin's source
+// position in fp64 (cos g, sin g from the plan's fp64 table of the 360 angles, exact at
+// multiples of 90) plus an fp32 offset of <= 40 px per pixel, then 4 bilinear taps per
+// image through the read-only path.  It writes, as requested:
 //   * the plain rotated image out[b][r][c]                          (skei_rotate's output)
 //   * the row-packed copy  xr[grp][r / R][c][r % R][b]  (R = 32 / BB lines per block)
 //   * the col-packed copy  xc[grp][c / R][r][c % R][b]
@@ -18,115 +19,127 @@
 namespace skei {
 namespace {
 
-constexpr int kTR = 8, kTC = 32;  // tile rows x columns
+constexpr int kT = 32;          // tile side (pixels)
+constexpr int kThreads = 256;   // 32 columns x 8 row groups; a thread owns 4 rows
+
+struct RotOrigin {
+    int bc, br;      // integer part of the tile origin's source column / row
+    float fc, fr;    // fractional parts
+    float cg, sg;    // cos g, sin g
+};
 
 template <int BB>
-__global__ void __launch_bounds__(kTR * kTC) k_rotate_pack(RotPackArgs a) {
+struct VecT;
+template <> struct VecT<1> { using T = float; };
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<4> { using T = float4; };
+
+template <int BB>
+__global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     constexpr int R = 32 / BB;
-    constexpr int kRow = kTC * BB + 4;  // padded tile row (floats): conflict-free pack reads
-    __shared__ __align__(16) float tile[kTR * kRow];
+    using V = typename VecT<BB>::T;
+    constexpr int kRow = kT * BB + 4;  // padded tile row (floats)
+    __shared__ __align__(16) float tile[kT * kRow];
+    __shared__ RotOrigin sRot[BB];
     const RotPackJob job = blockIdx.z ? a.job[1] : a.job[0];
     const int n = a.n;
-    const int tr = threadIdx.x / kTC, tc = threadIdx.x % kTC;
-    const int r0 = blockIdx.x / a.tiles_c * kTR, c0 = blockIdx.x % a.tiles_c * kTC;
-    const int r = r0 + tr, c = c0 + tc;
+    const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
+    const int r0 = blockIdx.x / a.tiles_c * kT, c0 = blockIdx.x % a.tiles_c * kT;
     const int b0 = blockIdx.y * BB;
     const long nn = (long)n * n;
-    const bool inside = r < n && c < n;
     if (job.zero && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
         job.zero[0] = job.zero[1] = job.zero[2] = 0u;  // the pass's counters (fused
                                                         // reductions, forward work queue)
-
-    float v[BB];
-#pragma unroll
-    for (int b = 0; b < BB; ++b) v[b] = 0.f;
-    if (inside) {
-        if (job.g == nullptr) {  // identity (pack x1)
-#pragma unroll
-            for (int b = 0; b < BB; ++b)
-                if (b0 + b < a.B) v[b] = __ldg(job.x + (b0 + b) * nn + (long)r * n + c);
-        } else {
-            // fp64 source coordinates, once per pixel for a shared g (g_stride = 0) or per
-            // image (g_stride = 1)
-            const double h = (n - 1) * 0.5;
-            const double u = c - h, w = h - r;
-            int gprev = 0x7fffffff;
-            float w00 = 0.f, w01 = 0.f, w10 = 0.f, w11 = 0.f;
-            bool okr0 = false, okr1 = false, okc0 = false, okc1 = false;
-            long o00 = 0;
-#pragma unroll
-            for (int b = 0; b < BB; ++b) {
-                if (b0 + b >= a.B) continue;
-                const int gd = job.g[job.g_stride ? b0 + b : 0];
-                if (gd != gprev) {
-                    gprev = gd;
-                    // (cos g, sin g) from the plan's fp64 table (exact at multiples of 90)
-                    const double2 csg = a.rot[((gd % 360) + 360) % 360];
-                    const double cg = csg.x, sg = csg.y;
-                    const double us = u * cg + w * sg;
-                    const double vs = -u * sg + w * cg;
-                    const double cs = us + h, rs = h - vs;
-                    const double r0d = floor(rs), c0d = floor(cs);
-                    const float fa = (float)(rs - r0d), fb = (float)(cs - c0d);
-                    const int ri = (int)r0d, ci = (int)c0d;
-                    okr0 = ri >= 0 && ri < n;
-                    okr1 = ri + 1 >= 0 && ri + 1 < n;
-                    okc0 = ci >= 0 && ci < n;
-                    okc1 = ci + 1 >= 0 && ci + 1 < n;
-                    w00 = (1.f - fa) * (1.f - fb);
-                    w01 = (1.f - fa) * fb;
-                    w10 = fa * (1.f - fb);
-                    w11 = fa * fb;
-                    o00 = (long)ri * n + ci;
-                }
-                const float *xb = job.x + (b0 + b) * nn;
-                float acc = 0.f;
-                if (okr0 && okc0) acc = fmaf(w00, __ldg(xb + o00), acc);
-                if (okr0 && okc1) acc = fmaf(w01, __ldg(xb + o00 + 1), acc);
-                if (okr1 && okc0) acc = fmaf(w10, __ldg(xb + o00 + n), acc);
-                if (okr1 && okc1) acc = fmaf(w11, __ldg(xb + o00 + n + 1), acc);
-                v[b] = acc;
-            }
-        }
-        if (job.out) {
-#pragma unroll
-            for (int b = 0; b < BB; ++b)
-                if (b0 + b < a.B) job.out[(b0 + b) * nn + (long)r * n + c] = v[b];
-        }
-    }
-    if (!job.xr && !job.xc) return;
-    {
-        float *tp = tile + tr * kRow + tc * BB;
-        if constexpr (BB == 4) {
-            *reinterpret_cast<float4 *>(tp) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
-#pragma unroll
-            for (int b = 0; b < BB; ++b) tp[b] = v[b];
-        }
+    if (job.g != nullptr && threadIdx.x < BB && b0 + (int)threadIdx.x < a.B) {
+        // source position of the tile origin (r0, c0) for image b0 + threadIdx.x, in fp64:
+        // c' = h + (c0 - h) cos g + (h - r0) sin g,  r' = h + (c0 - h) sin g - (h - r0) cos g
+        const int gd = job.g[job.g_stride ? b0 + threadIdx.x : 0];
+        const double2 csg = a.rot[((gd % 360) + 360) % 360];  // exact at multiples of 90
+        const double h = (n - 1) * 0.5, u = c0 - h, w = h - r0;
+        const double cs = h + u * csg.x + w * csg.y;
+        const double rs = h + u * csg.y - w * csg.x;
+        const double fc = floor(cs), fr = floor(rs);
+        sRot[threadIdx.x] = RotOrigin{(int)fc, (int)fr, (float)(cs - fc), (float)(rs - fr),
+                                      (float)csg.x, (float)csg.y};
     }
     __syncthreads();
-    const long grp_stride = (long)a.nblk * n * 32;  // floats per image group per class
-    const int e = threadIdx.x;                    // 256 threads, one float each per pass
-    if (job.xr) {
-        // row-packed: for each tile column c, the tile's rows are consecutive line slots of
-        // their block (R >= 8: one block, 8 x BB contiguous floats)
-        float *dst = job.xr + blockIdx.y * grp_stride;
-        for (int q = e; q < kTC * kTR * BB; q += kTR * kTC) {
-            const int b = q % BB, l = (q / BB) % kTR, cc = q / (BB * kTR);
-            const int row = r0 + l;
-            if (c0 + cc < n)
-                dst[((long)(row / R) * n + c0 + cc) * 32 + (row % R) * BB + b] =
-                    tile[l * kRow + cc * BB + b];
+
+    const int c = c0 + tc;
+#pragma unroll
+    for (int i = 0; i < kT / 8; ++i) {
+        const int rr = tr + 8 * i, r = r0 + rr;
+        float v[BB];
+#pragma unroll
+        for (int b = 0; b < BB; ++b) v[b] = 0.f;
+        if (r < n && c < n) {
+            if (job.g == nullptr) {  // identity (pack x1)
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    if (b0 + b < a.B) v[b] = __ldg(job.x + (b0 + b) * nn + (long)r * n + c);
+            } else {
+                // split-precision source coordinates: the tile origin's source position
+                // (fp64, sRot) plus an fp32 offset of at most 2 x 32 pixels
+                const float dr = (float)rr, dc = (float)tc;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) {
+                    if (b0 + b >= a.B) continue;
+                    const RotOrigin o = sRot[job.g_stride ? b : 0];
+                    const float cl = o.fc + fmaf(dc, o.cg, -dr * o.sg);
+                    const float rl = o.fr + fmaf(dc, o.sg, dr * o.cg);
+                    const float flc = floorf(cl), flr = floorf(rl);
+                    const float fb = cl - flc, fa = rl - flr;
+                    const int ci = o.bc + (int)flc, ri = o.br + (int)flr;
+                    const bool okr0 = ri >= 0 && ri < n, okr1 = ri + 1 >= 0 && ri + 1 < n;
+                    const bool okc0 = ci >= 0 && ci < n, okc1 = ci + 1 >= 0 && ci + 1 < n;
+                    const float *xb = job.x + (b0 + b) * nn + (long)ri * n + ci;
+                    float acc = 0.f;
+                    if (okr0 && okc0) acc = fmaf((1.f - fa) * (1.f - fb), __ldg(xb), acc);
+                    if (okr0 && okc1) acc = fmaf((1.f - fa) * fb, __ldg(xb + 1), acc);
+                    if (okr1 && okc0) acc = fmaf(fa * (1.f - fb), __ldg(xb + n), acc);
+                    if (okr1 && okc1) acc = fmaf(fa * fb, __ldg(xb + n + 1), acc);
+                    v[b] = acc;
+                }
+            }
+            if (job.out) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                    if (b0 + b < a.B) job.out[(b0 + b) * nn + (long)r * n + c] = v[b];
+            }
+        }
+        V t;
+        float *tp = reinterpret_cast<float *>(&t);
+#pragma unroll
+        for (int b = 0; b < BB; ++b) tp[b] = v[b];
+        *reinterpret_cast<V *>(tile + rr * kRow + tc * BB) = t;
+    }
+    if (!job.xr && !job.xc) return;
+    __syncthreads();
+    const long grp = (long)blockIdx.y * a.nblk * n * 32;  // floats per image group per class
+    const int lim = a.nblk * R;                            // packed lines (incl. zero padding)
+    // each item is one pixel-line slot of BB floats (16 / 8 / 4 bytes); consecutive threads
+    // take consecutive slots of a packed 128-byte pixel column
+    if (job.xr) {  // row-packed: block r / R, pixel c, line r % R
+        for (int it = threadIdx.x; it < kT * kT; it += kThreads) {
+            const int rl = it % R, rest = it / R;
+            const int cc = rest % kT, rb = rest / kT;  // rows rb*R .. +R-1 of the tile
+            const int rr = rb * R + rl;
+            if (rr >= kT) continue;
+            const int r = r0 + rr, cg = c0 + cc;
+            if (r < lim && cg < n)
+                *reinterpret_cast<V *>(job.xr + grp + ((long)(r / R) * n + cg) * 32 + (r % R) * BB) =
+                    *reinterpret_cast<const V *>(tile + rr * kRow + cc * BB);
         }
     }
-    if (job.xc) {
-        // col-packed: block c/R holds columns [R*(c/R), +R); rows r0..r0+7 of the tile are
-        // contiguous pixel entries of 32 floats, of which this tile fills columns c0..c0+31
-        float *dst = job.xc + blockIdx.y * grp_stride;
-        for (int q = e; q < kTR * kTC * BB; q += kTR * kTC) {
-            const int b = q % BB, cc = (q / BB) % kTC, l = q / (BB * kTC);
-            const int col = c0 + cc, row = r0 + l;
-            if (row < n && col < a.nblk * R) dst[((long)(col / R) * n + row) * 32 + (col % R) * BB + b] = tile[l * kRow + cc * BB + b];
+    if (job.xc) {  // col-packed: block c / R, pixel r, line c % R
+        for (int it = threadIdx.x; it < kT * kT; it += kThreads) {
+            const int cl = it % R, rest = it / R;
+            const int rr = rest % kT, cb = rest / kT;
+            const int cc = cb * R + cl;
+            if (cc >= kT) continue;
+            const int r = r0 + rr, cg = c0 + cc;
+            if (r < n && cg < lim)
+                *reinterpret_cast<V *>(job.xc + grp + ((long)(cg / R) * n + r) * 32 + (cg % R) * BB) =
+                    *reinterpret_cast<const V *>(tile + rr * kRow + cc * BB);
         }
     }
 }
@@ -149,15 +162,14 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
     a.rot = plan->d_rot;
     const int R = 32 / bb;
     a.nblk = (plan->n + R - 1) / R;
-    a.tiles_c = (plan->n + kTC - 1) / kTC;
-    // rows: cover whole packed blocks (multiples of R) so padding lines are zero-filled
-    const int rows = a.nblk * R;
-    const int tiles_r = (rows + kTR - 1) / kTR;
-    dim3 grid((unsigned)(tiles_r * a.tiles_c), (unsigned)((B + bb - 1) / bb), (unsigned)njobs);
+    // tiles cover the image and every packed line (incl. the zero padding lines)
+    const int side = a.nblk * R > plan->n ? a.nblk * R : plan->n;
+    a.tiles_c = (side + kT - 1) / kT;
+    dim3 grid((unsigned)(a.tiles_c * a.tiles_c), (unsigned)((B + bb - 1) / bb), (unsigned)njobs);
     switch (bb) {
-        case 4: k_rotate_pack<4><<<grid, kTR * kTC, 0, s>>>(a); break;
-        case 2: k_rotate_pack<2><<<grid, kTR * kTC, 0, s>>>(a); break;
-        default: k_rotate_pack<1><<<grid, kTR * kTC, 0, s>>>(a); break;
+        case 4: k_rotate_pack<4><<<grid, kThreads, 0, s>>>(a); break;
+        case 2: k_rotate_pack<2><<<grid, kThreads, 0, s>>>(a); break;
+        default: k_rotate_pack<1><<<grid, kThreads, 0, s>>>(a); break;
     }
     return cudaGetLastError();
 }
