@@ -46,6 +46,11 @@ def parse():
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
     ap.add_argument("--mode", default="uniform", choices=["uniform", "interleaved"])
+    ap.add_argument("--split", default="batch", choices=["batch", "angle"],
+                    help="batch: every rank runs its own batch (weak scaling, no collective); "
+                         "angle: one batch, the sketch's angles split over the ranks with one "
+                         "NCCL all-reduce of the partial backprojections (strong scaling, "
+                         "BASELINE cfg5)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -176,10 +181,84 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU leg
+def run_angle(args):
+    """--split angle: one batch (default cfg5, a single 1024^2 image), its m sketch angles
+    split over the ranks (dist.angle_split_pass); one all_reduce(SUM) of [x_fbp | grad | mc]
+    per step over NCCL.  Strong scaling: value = passes/s of the whole job."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_05771_b200 as sk
+    from paper_2411_05771_b200 import dist as skdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    mode = sk.MODE_UNIFORM if args.mode == "uniform" else sk.MODE_INTERLEAVED
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len, device=local)
+    x1_np, y_np = synth.make_workload(cfg, args.seed)
+    x1 = torch.from_numpy(x1_np).to(dev)
+    y = torch.from_numpy(y_np).to(dev)
+    ops = skdist.CudaOps(plan)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(it):
+        g, idx = sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, cfg.m, mode)
+        return skdist.angle_split_pass(ops, x1, y, g, idx[0])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = mk(), mk()
+            a.record()
+            out = step(args.warmup + i)
+            b.record()
+            times.append((a, b))
+        torch.cuda.synchronize()
+    total_ms = float(sum(a.elapsed_time(b) for a, b in times))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": f"sketched EI operator passes/s, {cfg.name} ({cfg.N}^2, {cfg.n_full}->{cfg.m} "
+                      f"angles) split by angle", "value": args.steps / (total_ms * 1e-3),
+            "unit": "passes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {**workload_desc(cfg, args.mode), "parallelism": f"angle split x{world}",
+                       "allreduce_bytes": int(out["allreduce_bytes"]),
+                       "launch": "direct (not graphed): 8 library calls + 1 NCCL all-reduce"},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.split == "angle":
+        if args.config == "cfg3" and "--config" not in sys.argv:
+            args.config = "cfg5"
+        return run_angle(args)
 
     import torch
     import torch.distributed as dist

@@ -169,7 +169,8 @@ skei_status skei_fbp(const skei_plan *plan, const float *p, float *x, int32_t B,
  * unnormalised squared l2 norms, R15).  p1: [B][m][n_det] (= A_S x1);
  * y: [B][n_full][n_det] full measured sinogram; x2, x3: [B][n][n]; mc, ei: [B];
  * r: [B][m][n_det] or NULL (not written).  Two-stage deterministic reduction.
- * ws as skei_fbp. */
+ * Either part may be skipped: p1 = y = mc = NULL computes only ei (idx then only sizes
+ * the workspace), x2 = x3 = ei = NULL only r and mc.  ws as skei_fbp. */
 skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float *y,
                              const int32_t *idx, int32_t m, int32_t idx_stride,
                              const float *x2, const float *x3, int32_t B,

@@ -257,9 +257,14 @@ def fbp(plan: Plan, p: torch.Tensor, idx: torch.Tensor, m_total: int | None = No
 
 def ei_residual(plan: Plan, p1, y, idx, x2, x3, r: torch.Tensor | None = None, want_r: bool = True,
                 ws: torch.Tensor | None = None):
-    B, m = p1.shape[0], p1.shape[1]
-    mc = torch.empty(B, dtype=torch.float32, device=p1.device)
-    ei = torch.empty(B, dtype=torch.float32, device=p1.device)
+    """(mc, ei, r).  p1 = y = None computes only ei; x2 = x3 = None only (mc, r)."""
+    ref = p1 if p1 is not None else x2
+    B, m = ref.shape[0], idx.shape[-1]
+    dev = ref.device
+    mc = torch.empty(B, dtype=torch.float32, device=dev) if p1 is not None else None
+    ei = torch.empty(B, dtype=torch.float32, device=dev) if x2 is not None else None
+    if p1 is None:
+        want_r = False
     if want_r and r is None:
         r = torch.empty_like(p1)
     ws = plan.workspace(B, m) if ws is None else ws
@@ -267,7 +272,7 @@ def ei_residual(plan: Plan, p1, y, idx, x2, x3, r: torch.Tensor | None = None, w
                                   _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
                                   _ptr(x2, name="x2"), _ptr(x3, name="x3"), B, _ptr(mc), _ptr(ei),
                                   _ptr(r) if want_r else None, _ptr(ws, torch.uint8, "ws"),
-                                  ws.numel(), _stream(p1)), "skei_ei_residual")
+                                  ws.numel(), _stream(ref)), "skei_ei_residual")
     return mc, ei, r
 
 

@@ -340,12 +340,16 @@ skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float
                              skei_stream stream) {
     skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
     if (st != SKEI_OK) return st;
-    if (!p1 || !y || !x2 || !x3 || !mc || !ei || !ws) return SKEI_ERR_ARG;
+    const bool do_mc = p1 || y || mc, do_ei = x2 || x3 || ei;
+    if (!ws || (!do_mc && !do_ei)) return SKEI_ERR_ARG;
+    if (do_mc && (!p1 || !y || !mc)) return SKEI_ERR_ARG;  // the MC part needs all three
+    if (do_ei && (!x2 || !x3 || !ei)) return SKEI_ERR_ARG;  // the EI part needs all three
     if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
     void *w = ws_f(ws, ws_layout(plan, B, m).res);
-    SKEI_CUDA(launch_residual(plan, p1, y, idx, m, idx_stride, x2, x3, B, mc, ei, r, w,
-                              (cudaStream_t)stream));
+    SKEI_CUDA(launch_residual(plan, do_mc ? p1 : nullptr, y, idx, m, idx_stride,
+                              do_ei ? x2 : nullptr, x3, B, do_mc ? mc : nullptr,
+                              do_ei ? ei : nullptr, do_mc ? r : nullptr, w, (cudaStream_t)stream));
     return SKEI_OK;
 }
 

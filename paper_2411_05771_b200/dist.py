@@ -1,0 +1,135 @@
+"""Multi-GPU partitioning of the sketched-EI operator pass.
+
+One process per GPU (torchrun), torch.distributed for the plumbing.  Two partitions:
+
+* batch split (BASELINE.json cfg4, "split by batch across 1/2/4/8 GPUs"): rank r owns the
+  global images [r B/G, (r+1) B/G).  Images are independent and the draws are keyed by the
+  global image index (R5), so every rank runs the whole pass on its images with no
+  data-path collective; results equal the 1-GPU run bit for bit.
+* angle split (cfg5, "single image ... split by angle ... with NCCL all-reduce of partial
+  backprojections"): rank r owns the contiguous slice S_r of the sketch's m angles.  Every
+  operator of the pass is a sum over angles except the rotation and the EI norm, so
+
+      x_fbp = (pi / 2m) A_S^T ramp(A_S x2) = sum_r (pi / 2m) A_{S_r}^T ramp(A_{S_r} x2)
+      grad  = 2 A_S^T (A_S x1 - y_S)        = sum_r 2 A_{S_r}^T r_r
+      mc    = ||A_S x1 - y_S||^2            = sum_r ||r_r||^2
+
+  (the sketch is a row subset; §1.1: ||Ax - y||^2 = sum_i ||S_i A x -
+  S_i y||^2).  Each rank computes its partials with the FBP density scale of the FULL
+  sketch size m (skei_fbp's m_total), packs [x_fbp | grad | mc] into one buffer, and one
+  all_reduce(SUM) over NVLink/NVSwitch completes them; ei = ||x2 - x_fbp||^2 is then
+  evaluated on the summed x_fbp (redundantly on every rank).
+
+The compute is injected (`ops`): `CudaOps` calls the C ABI (libskei.so); the CPU tests pass
+an oracle-backed implementation so the partition logic runs under gloo without a GPU.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+__all__ = ["batch_range", "angle_shard", "CudaOps", "angle_split_pass", "batch_split_images"]
+
+
+def batch_range(B: int, rank: int, world: int) -> range:
+    """Global image indices of `rank` when B images are split over `world` ranks (contiguous,
+    sizes differ by at most one)."""
+    if B < 1 or world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad split B={B} rank={rank} world={world}")
+    q, rem = divmod(B, world)
+    lo = rank * q + min(rank, rem)
+    return range(lo, lo + q + (1 if rank < rem else 0))
+
+
+def batch_split_images(x: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    r = batch_range(x.shape[0], rank, world)
+    return x[r.start:r.stop]
+
+
+def angle_shard(idx, rank: int, world: int):
+    """The contiguous slice of the sketch (m ascending angle indices) owned by `rank`."""
+    m = len(idx)
+    if m < world:
+        raise ValueError(f"angle split needs m >= world ({m} < {world})")
+    r = batch_range(m, rank, world)
+    return idx[r.start:r.stop]
+
+
+@dataclass
+class CudaOps:
+    """The pass's operators on one GPU, through the C ABI (paper_2411_05771_b200)."""
+    plan: object
+
+    def rotate(self, x1, g):
+        import paper_2411_05771_b200 as sk
+        return sk.rotate(self.plan, x1, g)
+
+    def forward(self, x, idx):
+        import paper_2411_05771_b200 as sk
+        return sk.radon_fwd(self.plan, x, idx)
+
+    def residual(self, p1, y, idx):
+        import paper_2411_05771_b200 as sk
+        mc, _, r = sk.ei_residual(self.plan, p1, y, idx, None, None)
+        return mc, r
+
+    def fbp(self, p2, idx, m_total, out=None):
+        import paper_2411_05771_b200 as sk
+        return sk.fbp(self.plan, p2, idx, m_total=m_total, out=out)
+
+    def adjoint(self, r, idx, scale, out=None):
+        import paper_2411_05771_b200 as sk
+        return sk.radon_adj(self.plan, r, idx, scale, out=out)
+
+    def ei(self, x2, x3, idx):
+        import paper_2411_05771_b200 as sk
+        _, ei, _ = sk.ei_residual(self.plan, None, None, idx, x2, x3)
+        return ei
+
+
+def angle_split_pass(ops, x1, y, g, idx, group=None):
+    """One sketched-EI pass of a batch whose sketch `idx` (m ascending indices) is split over
+    the ranks of `group` (the whole world if None).  Returns a dict with x2, x_fbp, grad
+    (complete on every rank after the all-reduce), mc and ei ([B]), and this rank's p1, p2, r
+    shards with their angle indices.  Single-rank groups reduce to the plain pass."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    m = len(idx)
+    sub = angle_shard(idx, rank, world)
+    x2 = ops.rotate(x1, g)
+    p1 = ops.forward(x1, sub)
+    p2 = ops.forward(x2, sub)
+    B, N = x1.shape[0], x1.shape[-1]
+    nn = B * N * N
+    # one packed buffer [x_fbp (B N^2) | grad (B N^2) | mc (B)]: the kernels write their
+    # partials straight into it, then one all_reduce(SUM) completes all three
+    packed = torch.empty(2 * nn + B, dtype=x1.dtype, device=x1.device)
+    xfbp = packed[:nn].view(B, N, N)
+    grad = packed[nn:2 * nn].view(B, N, N)
+    mc = packed[2 * nn:]
+    mc_part, r = ops.residual(p1, y, sub)
+    ops.fbp(p2, sub, m, out=xfbp)      # density scale pi / (2 m) of the FULL sketch
+    ops.adjoint(r, sub, 2.0, out=grad)
+    mc.copy_(mc_part)
+    if world > 1:
+        dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
+    ei = ops.ei(x2, xfbp, idx)
+    return {"x2": x2, "xfbp": xfbp, "grad": grad, "mc": mc, "ei": ei,
+            "p1": p1, "p2": p2, "r": r, "idx": sub, "allreduce_bytes": packed.numel() * packed.element_size()}
+
+
+def allreduce_bytes(B: int, N: int) -> int:
+    """Bytes of the angle split's single all-reduce: (2 B N^2 + B) fp32."""
+    return 4 * (2 * B * N * N + B)
+
+
+def ring_bytes_per_gpu(B: int, N: int, world: int) -> float:
+    """Bytes each GPU sends in a ring all-reduce of the packed buffer: 2 (G-1)/G x payload."""
+    return 2.0 * (world - 1) / world * allreduce_bytes(B, N) if world > 1 else 0.0
+
+
+def expected_scale(m_total: int) -> float:
+    return math.pi / (2.0 * m_total)
