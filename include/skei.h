@@ -206,11 +206,13 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const skei_pass_outputs *out, float *h_mc, float *h_ei,
                            void *ws, size_t ws_bytes, skei_stream stream);
 
-/* skei_pass with stage timing: `events` holds n_events (>= 7) cudaEvent_t handles
- * created by the caller; event 0 is recorded before the first stage and event i after
- * stage i of: 1 rotate, 2 forward (A_S x1 and A_S x2, one launch), 3 ramp,
- * 4 residual r/mc, 5 the two backprojections (FBP and gradient, one launch),
- * 6 residual ei.  Otherwise identical to skei_pass (same launches, same results). */
+/* skei_pass with stage timing: `events` holds n_events (>= 6) cudaEvent_t handles
+ * created by the caller, NULL entries skipped; event 0 is recorded before the first stage
+ * and event i after stage i of: 1 rotate + packing, 2 forward (A_S x1 with the fused MC
+ * residual, and A_S x2: one launch), 3 ramp, 4 the two backprojections (FBP and gradient,
+ * one launch, with the fused EI residual), 5 end.  Under stream capture the events
+ * become external event-record nodes.  Otherwise identical to skei_pass with x3 = NULL
+ * (same launches, same results). */
 skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1,
                                const float *y, const int32_t *g_deg, int32_t g_stride,
                                const int32_t *idx, int32_t m, int32_t idx_stride,

@@ -306,14 +306,17 @@ def sketched_pass(plan: Plan, x1, y, g, idx, x3=None, out: dict | None = None,
 
 
 def sketched_pass_profiled(plan: Plan, x1, y, g, idx, events, out: dict, ws: torch.Tensor):
-    """skei_pass_profiled: skei_pass with 7 caller-owned torch.cuda.Events recorded around
-    its 6 stages (rotate, forward x2, ramp, residual mc, backprojection x2, residual ei)."""
+    """skei_pass_profiled: skei_pass with up to 6 caller-owned torch.cuda.Events (None =
+    skipped) recorded at the stage boundaries: 0 start, 1 after rotate+pack, 2 after the
+    forward (with fused MC residual), 3 after the ramp, 4 after the backprojections (with
+    fused EI residual), 5 end."""
     B, m = x1.shape[0], idx.shape[-1]
     po = _pass_out(out)
     for e in events:  # torch creates the cudaEvent_t lazily, on its first record()
-        if e.cuda_event == 0:
+        if e is not None and e.cuda_event == 0:
             e.record()
-    ev = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    ev = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event if e is not None else 0)
+                                            for e in events])
     _check(lib().skei_pass_profiled(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
                                     _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,
                                     _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),

@@ -378,8 +378,8 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
         SKEI_CUDA(cudaStreamIsCapturing(s, &cs));
         if (cs == cudaStreamCaptureStatusActive) ev_flags = cudaEventRecordExternal;
     }
-    auto mark = [&](int i) -> cudaError_t {
-        return ev ? cudaEventRecordWithFlags(ev[i], s, ev_flags) : cudaSuccess;
+    auto mark = [&](int i) -> cudaError_t {  // NULL slots are skipped
+        return (ev && ev[i]) ? cudaEventRecordWithFlags(ev[i], s, ev_flags) : cudaSuccess;
     };
     const float fbp_scale = (float)(M_PI / (2.0 * m));
 
@@ -403,17 +403,16 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     // a4: q = ramp(p2)
     SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s));
     SKEI_CUDA(mark(3));
-    SKEI_CUDA(mark(4));  // (the MC residual ran inside the forward launch)
     // a5 + a8 (+ a7 EI part when x3 is the identity network's x_fbp): x_fbp = (pi/2m) A_S^T q
     // and grad = 2 A_S^T r in one launch, ei = ||x2 - x_fbp||^2 fused into its epilogue
     AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale}, {o->r, o->grad, 2.0f}};
     AdjEi eif{o->x2, ws_f(ws, wl.eipart), ctr + 1, o->ei};
     SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, x3_in ? nullptr : &eif));
-    SKEI_CUDA(mark(5));
+    SKEI_CUDA(mark(4));
     if (x3_in)  // a7 (EI part) against a caller-provided x3
         SKEI_CUDA(launch_residual(plan, nullptr, nullptr, idx, m, idx_stride, o->x2, x3_in, B,
                                   nullptr, o->ei, nullptr, wres, s));
-    SKEI_CUDA(mark(6));
+    SKEI_CUDA(mark(5));
     return SKEI_OK;
 }
 
@@ -432,9 +431,7 @@ skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1
                                const int32_t *idx, int32_t m, int32_t idx_stride,
                                const skei_pass_outputs *out, void *ws, size_t ws_bytes,
                                void *const *events, int32_t n_events, skei_stream stream) {
-    if (!events || n_events < 7) return SKEI_ERR_ARG;
-    for (int i = 0; i < 7; ++i)
-        if (!events[i]) return SKEI_ERR_ARG;
+    if (!events || n_events < 6) return SKEI_ERR_ARG;
     return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, nullptr, out, ws,
                     ws_bytes, (cudaEvent_t const *)events, (cudaStream_t)stream);
 }

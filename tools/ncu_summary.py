@@ -75,6 +75,10 @@ def main():
         rd, _ = value(r, hdr, units, "dram__bytes_read.sum")
         wr, _ = value(r, hdr, units, "dram__bytes_write.sum")
         traffic.setdefault(short, rd + wr)
+        for pre, stage in (("k_radon_fwd", "radon_fwd_x2"), ("k_radon_adj", "radon_adj_x2"),
+                           ("k_ramp", "ramp"), ("k_rotate_pack", "rotate_pack")):
+            if short.startswith(pre):
+                traffic.setdefault(stage, rd + wr)
     if "--traffic" in sys.argv:
         path = sys.argv[sys.argv.index("--traffic") + 1]
         json.dump(traffic, open(path, "w"), indent=1)
