@@ -355,6 +355,8 @@ def main():
         torch.cuda.synchronize()
     step_ms = np.array([a.elapsed_time(c) for a, _, c in recs])
     fwd_ms = np.array([evs[1].elapsed_time(evs[2]) for _, evs, _ in recs])
+    if os.environ.get("SKEI_BENCH_DUMP"):  # diagnostics: per-step forward times
+        sys.stderr.write("fwd_us " + " ".join(f"{v * 1e3:.0f}" for v in fwd_ms) + "\n")
     total_ms = float(step_ms.sum())
     # stage breakdown (untimed replays of the fully instrumented graphs)
     brk = []

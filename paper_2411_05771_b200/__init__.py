@@ -35,7 +35,7 @@ MODE_INTERLEAVED, MODE_UNIFORM = 0, 1
 SHARED_IMAGE = (1 << 64) - 1
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libskei.so")
+lib_path = os.environ.get("SKEI_LIB") or os.path.join(_HERE, "libskei.so")  # override: A/B diagnostics
 _lib = None
 _lock = threading.Lock()
 

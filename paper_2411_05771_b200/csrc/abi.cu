@@ -72,8 +72,8 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
         w.pack[i] = off;
         off += align256(sizeof(float) * pk);
     }
-    w.ctr = off;  // 2 completion counters of the fused reductions
-    off += 256;
+    w.ctr = off;  // completion counters of the fused reductions + forward split units
+    off += align256(sizeof(unsigned) * kPassCounters);
     w.mcpart = off;
     off += align256(sizeof(float) * (size_t)B * fwd_mc_slots(plan, B, m, 0));
     w.eipart = off;
@@ -190,7 +190,7 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     p->fft_len = P;
     p->log2_fft = 0;
     while ((1 << p->log2_fft) < P) ++p->log2_fft;
-    p->num_sms = prop.multiProcessorCount;
+    p->num_sms = prop.multiProcessorCount < 256 ? prop.multiProcessorCount : 256;  // kPassCounters
     cudaError_t e = cudaMalloc(&p->d_trig, sizeof(double2) * n_full);
     if (e == cudaSuccess) e = cudaMalloc(&p->d_ramp, sizeof(float) * P);
     p->fft_npass = npass;

@@ -53,8 +53,11 @@ struct RotPackJob {
     const int32_t *g;    // rotation (device) or NULL = identity
     int g_stride;        // 0 shared, 1 per image
     float *xr, *xc;      // row- / col-packed outputs or NULL
-    unsigned *zero;      // if set, block (0,0,0) zeroes zero[0..2] (pass counters)
+    unsigned *zero;      // if set, block (0,0,0) zeroes zero[0..kPassCounters) (pass counters)
 };
+// Pass counters: [0] MC completion, [1] EI completion, [2..] the forward's stream-K split-unit
+// piece counters (one per cluster, <= 256 SMs).
+constexpr int kPassCounters = 2 + 256;
 struct RotPackArgs {
     RotPackJob job[2];
     const double2 *rot;  // plan->d_rot

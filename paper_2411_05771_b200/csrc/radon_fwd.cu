@@ -79,8 +79,10 @@ struct FwdArgs {
     int mc_slots;
     unsigned *mc_ctr;
     float *mc_out;
-    unsigned *queue;  // work-queue counter (zero before the launch)
-    float *scratch;   // per-CTA partial projections [gridDim.x][K * n_det * BB]
+    unsigned *queue;  // piece counters of the stream-K split units, indexed by the unit's
+                      // first cluster (< gridDim.x; zero before the launch, self-resetting)
+    float *scratch;   // per-CTA partial projections [gridDim.x][K * n_det * BB], then the
+                      // split-unit pieces [clusters][2][K * n_det * BB]
 };
 
 // ---- TMA bulk copy + mbarrier (sm_90+ async proxy), inline PTX
@@ -166,6 +168,18 @@ __device__ __forceinline__ void ldcg_vec(const float *p, float (&v)[BB]) {
     }
 }
 
+// L2 (st.global.cg) store of BB consecutive floats
+template <int BB>
+__device__ __forceinline__ void stg_vec(float *p, const float (&v)[BB]) {
+    if constexpr (BB == 4) {
+        __stcg(reinterpret_cast<float4 *>(p), make_float4(v[0], v[1], v[2], v[3]));
+    } else if constexpr (BB == 2) {
+        __stcg(reinterpret_cast<float2 *>(p), make_float2(v[0], v[1]));
+    } else {
+        __stcg(p, v[0]);
+    }
+}
+
 // Work decomposition shared by every CTA: for each image group q, nrow[q] = angles of its
 // sketch in the row class; units of q = ceil(nrow/K) + ceil((m - nrow)/K); uoff = prefix.
 struct Units {
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
     __shared__ float s_red[kWarps][BB];
     __shared__ bool s_last;
-    __shared__ int s_units[4];  // ring of this cluster's next units (grabbed one unit ahead)
+    __shared__ int s_fin;       // split unit: this cluster sums the pieces (0/1)
 
     cg::cluster_group cluster = cg::this_cluster();
     const int S = (int)cluster.num_blocks();
@@ -264,38 +278,59 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __syncthreads();
     const Units U{s_uoff, s_nrow, s_uoff[nq]};
     const int total_units = a.njobs * U.per_job;
-    // dynamic unit queue: the cluster leader grabs units (global counter) one unit ahead and
-    // the other ranks read them through DSMEM after the cluster barriers
-    if (rank == 0 && threadIdx.x == 0) {
-        s_units[0] = (int)atomicAdd(a.queue, 1u);
-        s_units[1] = (int)atomicAdd(a.queue, 1u);
-    }
-    cluster.sync();
-    if (rank != 0 && threadIdx.x < 2) s_units[threadIdx.x] = cluster.map_shared_rank(s_units, 0)[threadIdx.x];
-    __syncthreads();
-
-    // this CTA's lines: the same whole packed blocks in every unit
-    const int blocks_per = (a.nblk + S - 1) / S;
-    const int blk0 = min(a.nblk, rank * blocks_per), blk1 = min(a.nblk, blk0 + blocks_per);
-    const int nb = blk1 - blk0;
-    // this CTA's block stream: block g belongs to local unit g / nb; it exists if that unit
-    // is known (at most one unit ahead) and valid
-    auto block_ok = [&](int g) -> bool {
-        return nb > 0 && s_units[(g / nb) & 3] < total_units;
+    // ---- stream-K work split: the work is W = U x nbc cluster-blocks (nbc = ceil(nblk / S)
+    // line blocks per CTA per unit); cluster c takes the contiguous range [w(c), w(c+1)),
+    // w(c) = c W / ncl, so every cluster gets the same number of blocks whatever U is.  A unit
+    // cut by a range boundary is computed in pieces by consecutive clusters: each piece's
+    // (cluster-summed) partial goes to an L2 slot, and the last piece to finish (per-unit
+    // counter) adds the pieces in cluster order and finishes the unit.
+    const int nbc = (a.nblk + S - 1) / S;
+    const long W = (long)total_units * nbc;
+    auto wstart = [&](int c) -> long { return (long)c * W / ncl; };
+    const long w0 = wstart(cid), w1 = wstart(cid + 1);
+    const int u_first = (int)(w0 / nbc), u_last = w1 > w0 ? (int)((w1 - 1) / nbc) : u_first - 1;
+    auto cluster_of = [&](long w) -> int {  // the cluster whose range holds cluster-block w
+        int c = (int)(w * ncl / W);
+        while (c + 1 < ncl && wstart(c + 1) <= w) ++c;
+        while (c > 0 && wstart(c) > w) --c;
+        return c;
     };
+    float *pieces = a.scratch + (long)gridDim.x * part_f;  // [ncl][2][part_f]
+
+    // this CTA's lines and its blocks of unit u: [blk0 + lo, blk0 + hi)
+    const int blk0 = min(a.nblk, rank * nbc), blk1 = min(a.nblk, blk0 + nbc);
+    const int nb = blk1 - blk0;
+    auto unit_blocks = [&](int u, int &lo, int &hi) {
+        lo = (int)max(w0 - (long)u * nbc, 0L);
+        hi = (int)min(w1 - (long)u * nbc, (long)nbc);
+        lo = min(lo, nb);
+        hi = min(hi, nb);
+        if (hi < lo) hi = lo;
+    };
+    int G = 0;  // this CTA's block stream: its blocks of u_first .. u_last in order
+    for (int u = u_first; u <= u_last; ++u) {
+        int lo, hi;
+        unit_blocks(u, lo, hi);
+        G += hi - lo;
+    }
     auto block_src = [&](int g) -> const float * {
-        const int iu = g / nb, i = g - iu * nb;
-        const UnitId d = decode_unit(U, nq, K, s_units[iu & 3]);
-        const FwdJob &jb = d.job ? a.job[1] : a.job[0];
-        return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + blk0 + i) * n * kColF;
+        for (int u = u_first;; ++u) {
+            int lo, hi;
+            unit_blocks(u, lo, hi);
+            if (g < hi - lo) {
+                const UnitId d = decode_unit(U, nq, K, u);
+                const FwdJob &jb = d.job ? a.job[1] : a.job[0];
+                return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + blk0 + lo + g) * n * kColF;
+            }
+            g -= hi - lo;
+        }
     };
     // TMA pipeline: block g lives in buffer g % nbuf; blocks 0..nbuf-1 are issued up front,
     // block g + nbuf by the last warp to finish block g (shared counter), so warps are not
-    // barrier-synchronised per block and the stream runs on across unit boundaries (at
-    // most one unit ahead, hence nbuf <= nb).
-    const int nbuf = max(1, min(a.nbuf, nb));
+    // barrier-synchronised per block and the stream runs on across unit boundaries.
+    const int nbuf = max(1, min(a.nbuf, G));
     if (threadIdx.x == 0)
-        for (int g = 0; g < nbuf && g < 2 * nb && block_ok(g); ++g)
+        for (int g = 0; g < nbuf && g < G; ++g)
             issue_block(smem + g * stage_f + kPadL * kColF, block_src(g), n, &full[g]);
 
     // this lane's skewed line order l_s = (lane + s) mod R, as a float (position) and as a
@@ -311,9 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     const unsigned smem_b = smem_u32(smem);
     const unsigned cmax = (unsigned)(n + 3);
 
-    for (int iu = 0;; ++iu) {
-        const int u = s_units[iu & 3];
-        if (u >= total_units) break;  // same in every CTA of the cluster
+    int gbase = 0;  // stream index of the current unit's first block
+    for (int u = u_first; u <= u_last; ++u) {
+        int ulo, uhi;
+        unit_blocks(u, ulo, uhi);
+        const int nbu = uhi - ulo;  // this CTA's blocks of the unit
+        const bool full_unit = w0 <= (long)u * nbc && (long)(u + 1) * nbc <= w1;
         const UnitId d = decode_unit(U, nq, K, u);
         const FwdJob job = d.job ? a.job[1] : a.job[0];
         const int b0 = d.q * BB;
@@ -366,10 +404,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         // per (angle, block): the block's first-line position of bin 0, A = P0 + lb Pl, split
         // into (int base, fp32 frac) in fp64, and the exact range [jlo, jhi] of bins whose
         // candidates can fall inside the image for some line of the block
-        for (int e = threadIdx.x; e < kcnt * nb; e += kThreads) {
-            const int k = e / nb, i = e - k * nb;
+        for (int e = threadIdx.x; e < kcnt * nbu; e += kThreads) {
+            const int k = e / nbu, i = e - k * nbu;
             const double Pl = sPl[k], Pj = sPj[k];
-            const double A = sP0[k] + (double)((blk0 + i) * R) * Pl;
+            const double A = sP0[k] + (double)((blk0 + ulo + i) * R) * Pl;
             const double fA = floor(A);
             const double sec = 1.0 / (double)sAbsB[k];
             const double lmin = fmin(0.0, (R - 1) * Pl), lmax = fmax(0.0, (R - 1) * Pl);
@@ -406,9 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #pragma unroll
             for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
 
-        for (int i = 0; i < nb; ++i) {
-            const int g = iu * nb + i;
-            const int lb = (blk0 + i) * R;
+        for (int i = 0; i < nbu; ++i) {
+            const int g = gbase + i;
             const int cb = g % nbuf;
             const unsigned cur_b = smem_b + (unsigned)(cb * stage_f * sizeof(float));
             mbar_wait(&full[cb], (unsigned)((g / nbuf) & 1));
@@ -416,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             for (int t = 0; t < kMaxT; ++t) {
                 const int k = tk[t];
                 if (k < 0) break;  // warp-uniform
-                const int4 ent = btab[k * nb + i];
+                const int4 ent = btab[k * nbu + i];
                 if (tc[t] > ent.w || tc[t] + 31 < ent.z) continue;  // chunk misses the block
                 int base = ent.x + jb[t];
                 float frac = __int_as_float(ent.y) + jf[t];
@@ -466,8 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             if (lane == 0) {
                 __threadfence_block();  // this warp's reads of the buffer are complete
                 const int old = atomicAdd(&done[cb], 1);
-                if (old == kWarps * (g / nbuf + 1) - 1 && (g + nbuf) / nb <= iu + 1 &&
-                    block_ok(g + nbuf)) {
+                if (old == kWarps * (g / nbuf + 1) - 1 && g + nbuf < G) {
                     fence_proxy_async();  // generic-proxy reads -> async-proxy writes
                     issue_block(smem + cb * stage_f + kPadL * kColF, block_src(g + nbuf), n,
                                 &full[cb]);
@@ -487,49 +523,90 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
             }
         }
-        if (rank == 0 && threadIdx.x == 0) s_units[(iu + 2) & 3] = (int)atomicAdd(a.queue, 1u);
+        gbase += nbu;
         cluster.sync();  // partials of every rank written (cluster scope release/acquire)
-        if (rank != 0 && threadIdx.x == 0)
-            s_units[(iu + 2) & 3] = cluster.map_shared_rank(s_units, 0)[(iu + 2) & 3];
         const float *cpart = a.scratch + (long)(blockIdx.x - rank) * part_f;  // rank 0's
         // this rank's slice of the unit's (angle, bin) pairs; the S partials of a pair are one
         // BB-vector each, summed in rank order
         const int T2 = kcnt * n_det;
         const int per2 = (T2 + S - 1) / S;
         const int p0 = min(T2, rank * per2), p1 = min(T2, p0 + per2);
+        auto cluster_sum = [&](int o2, float (&sv)[BB]) {
+            float v[BB];
+            ldcg_vec<BB>(cpart + (long)o2 * BB, sv);
+            for (int q = 1; q < S; ++q) {
+                ldcg_vec<BB>(cpart + q * part_f + (long)o2 * BB, v);
+#pragma unroll
+                for (int b = 0; b < BB; ++b) sv[b] += v[b];
+            }
+        };
+        bool finish = full_unit;
+        const float *pc_first = nullptr;  // split unit: pieces of clusters c0 .. c1
+        int c0 = 0, c1 = -1;
+        if (!full_unit) {
+            // this cluster's piece -> its slot (0 if u is the cluster's first unit, else 1)
+            float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
+            for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
+                float sv[BB];
+                cluster_sum(o2, sv);
+                stg_vec<BB>(mine + (long)o2 * BB, sv);
+            }
+            __threadfence();
+            c0 = cluster_of((long)u * nbc);
+            c1 = cluster_of((long)u * nbc + nbc - 1);
+            int npc = 0;  // pieces = non-empty clusters c0 .. c1
+            for (int c = c0; c <= c1; ++c) npc += wstart(c + 1) > wstart(c);
+            cluster.sync();  // the whole piece written (and fenced) by every rank
+            if (rank == 0 && threadIdx.x == 0)
+                s_fin = atomicAdd(a.queue + c0, 1u) == (unsigned)(npc - 1) ? 1 : 0;
+            cluster.sync();
+            finish = cluster.map_shared_rank(&s_fin, 0)[0] != 0;
+            if (finish) {
+                __threadfence();
+                pc_first = pieces;
+            }
+        }
         const long img_stride = (long)a.m * n_det;
         const bool mc = job.y != nullptr;
         float racc[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) racc[b] = 0.f;
-        for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
-            const int k = o2 / n_det;
-            const int j = o2 - k * n_det;
-            const int slot = sSlot[k];
-            float sv[BB];
-            {
-                float v[BB];
-                ldcg_vec<BB>(cpart + (long)o2 * BB, sv);
-                for (int q = 1; q < S; ++q) {
-                    ldcg_vec<BB>(cpart + q * part_f + (long)o2 * BB, v);
+        if (finish) {
+            for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
+                const int k = o2 / n_det;
+                const int j = o2 - k * n_det;
+                const int slot = sSlot[k];
+                float sv[BB];
+                if (full_unit) {
+                    cluster_sum(o2, sv);
+                } else {  // the pieces of clusters c0 .. c1, in cluster order
 #pragma unroll
-                    for (int b = 0; b < BB; ++b) sv[b] += v[b];
+                    for (int b = 0; b < BB; ++b) sv[b] = 0.f;
+                    for (int c = c0; c <= c1; ++c) {
+                        if (wstart(c + 1) == wstart(c)) continue;  // empty range
+                        const int cslot = u == (int)(wstart(c) / nbc) ? 0 : 1;  // u first of c?
+                        float v[BB];
+                        ldcg_vec<BB>(pc_first + ((long)c * 2 + cslot) * part_f + (long)o2 * BB, v);
+#pragma unroll
+                        for (int b = 0; b < BB; ++b) sv[b] += v[b];
+                    }
+                }
+                const long pj = (long)slot * n_det + j;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
+                if (mc) {
+                    const long yj = (long)idx[slot] * n_det + j;
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) {
+                        const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
+                        if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
+                        racc[b] = fmaf(dr, dr, racc[b]);
+                    }
                 }
             }
-            const long pj = (long)slot * n_det + j;
-#pragma unroll
-            for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
-            if (mc) {
-                const long yj = (long)idx[slot] * n_det + j;
-#pragma unroll
-                for (int b = 0; b < BB; ++b) {
-                    const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
-                    if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
-                    racc[b] = fmaf(dr, dr, racc[b]);
-                }
-            }
+            if (!full_unit && rank == 0 && threadIdx.x == 0) a.queue[c0] = 0u;  // next launch
         }
-        if (mc) {  // per-(unit, rank) partial of each image of the group
+        if (mc && finish) {  // per-(unit, rank) partial of each image of the group
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
                 float v = racc[b];
@@ -538,8 +615,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (lane == 0) s_red[warp][b] = v;
             }
         }
-        cluster.sync();  // partials consumed, s_units ring updated everywhere; s_red complete
-        if (mc && threadIdx.x < BB) {
+        cluster.sync();  // partials consumed; s_red complete
+        if (mc && finish && threadIdx.x < BB) {
             float v = 0.f;
             for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
             const int slot = (u - U.uoff[d.q]) * S + rank;
@@ -595,10 +672,10 @@ int max_clusters(int S, size_t smem, int num_sms) {
     return ncl;
 }
 
-// Cluster size S (line split) of the persistent grid: ncl(S) co-resident clusters drain a
-// queue of `units`, each costing ceil(nblk / S) + 1 blocks per CTA (the +1 is the unit's
-// prologue/epilogue); with a dynamic queue the makespan is about units / ncl rounds plus half
-// a unit of tail.  SKEI_FWD_CLUSTER=S overrides the choice (tuning/diagnostics).
+// Cluster size S (line split) of the persistent grid: ncl(S) co-resident clusters share
+// `units`, each costing ceil(nblk / S) + 1 blocks per CTA (the +1 is the unit's
+// prologue/epilogue); stream-K splits the blocks evenly, so the makespan is about
+// units (ceil(nblk / S) + 1) / ncl blocks plus one split-unit epilogue.  SKEI_FWD_CLUSTER=S overrides the choice (tuning/diagnostics).
 template <int BB>
 int pick_cluster(long units, int nblk, int num_sms, size_t smem, int *ncl_out) {
     static int forced = -1;
@@ -611,7 +688,7 @@ int pick_cluster(long units, int nblk, int num_sms, size_t smem, int *ncl_out) {
     double best_cost = 1e30;
     for (int S = 1; S <= 8; ++S) {
         const int ncl = max_clusters<BB>(S, smem, num_sms);
-        const double cost = ((double)units / ncl + 0.5) * ((nblk + S - 1) / S + 1.0);
+        const double cost = (double)units * ((nblk + S - 1) / S + 1.0) / ncl + 1.0;
         if ((forced && S == forced) || (!forced && cost < best_cost - 1e-9)) {
             best_cost = cost;
             best = S;
@@ -663,8 +740,9 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
 }  // namespace
 
 size_t fwd_scratch_floats(const skei_plan *plan) {
-    // grid <= num_sms CTAs, each K * n_det * BB <= kWarps * kMaxT * 32 * 4 floats
-    return (size_t)plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
+    // grid <= num_sms CTAs, each K * n_det * BB <= kWarps * kMaxT * 32 * 4 floats, then two
+    // split-unit piece slots per cluster (<= num_sms clusters)
+    return (size_t)3 * plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
 }
 
 size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {

@@ -47,9 +47,8 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     const int r0 = blockIdx.x / a.tiles_c * kT, c0 = blockIdx.x % a.tiles_c * kT;
     const int b0 = blockIdx.y * BB;
     const long nn = (long)n * n;
-    if (job.zero && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-        job.zero[0] = job.zero[1] = job.zero[2] = 0u;  // the pass's counters (fused
-                                                        // reductions, forward work queue)
+    if (job.zero && blockIdx.x == 0 && blockIdx.y == 0)  // the pass's counters (fused
+        for (int t = threadIdx.x; t < kPassCounters; t += blockDim.x) job.zero[t] = 0u;  // reductions, forward split units)
     if (job.g != nullptr && threadIdx.x < BB && b0 + (int)threadIdx.x < a.B) {
         // source position of the tile origin (r0, c0) for image b0 + threadIdx.x, in fp64:
         // c' = h + (c0 - h) cos g + (h - r0) sin g,  r' = h + (c0 - h) sin g - (h - r0) cos g
