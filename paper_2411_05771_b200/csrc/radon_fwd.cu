@@ -168,6 +168,22 @@ __device__ __forceinline__ void ldcg_vec(const float *p, float (&v)[BB]) {
     }
 }
 
+// blk += w v over BB images, as packed fp32x2 FMAs (bitwise the same as scalar fmaf)
+template <int BB>
+__device__ __forceinline__ void fma_px(float (&blk)[BB], float w, const float (&v)[BB]) {
+    if constexpr (BB == 1) {
+        blk[0] = fmaf(w, v[0], blk[0]);
+    } else {
+        const float2 w2 = make_float2(w, w);
+#pragma unroll
+        for (int b = 0; b < BB; b += 2) {
+            const float2 r = __ffma2_rn(w2, make_float2(v[b], v[b + 1]), make_float2(blk[b], blk[b + 1]));
+            blk[b] = r.x;
+            blk[b + 1] = r.y;
+        }
+    }
+}
+
 // L2 (st.global.cg) store of BB consecutive floats
 template <int BB>
 __device__ __forceinline__ void stg_vec(float *p, const float (&v)[BB]) {
@@ -211,7 +227,9 @@ template <int BB>
 __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     constexpr int R = kColF / BB;
     constexpr int kMaxT = max_tasks<BB>();
-    extern __shared__ __align__(128) float smem[];  // nbuf stage buffers
+    extern __shared__ __align__(128) float smem_raw[];
+    // nbuf stage buffers from a 128-byte aligned base (the line-offset XOR below needs it)
+    float *smem = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
     __shared__ __align__(8) uint64_t full[3];
     __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
@@ -333,16 +351,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         for (int g = 0; g < nbuf && g < G; ++g)
             issue_block(smem + g * stage_f + kPadL * kColF, block_src(g), n, &full[g]);
 
-    // this lane's skewed line order l_s = (lane + s) mod R, as a float (position) and as a
-    // byte offset within a staged pixel column (minus 3 pad columns, see the clamp below)
-    float lfs[R];
-    unsigned lofs[R];
+    // this lane's line order: the s-th line visited is l = lane' ^ gray(s) (lane' = lane mod R,
+    // gray(s) = s ^ (s >> 1)), so the 32 / BB lanes of one shared-memory phase read R distinct
+    // lines (distinct bank groups) whatever pixels they hit, and consecutive lines differ in
+    // one bit i: the position e moves by +-2^i Pl (one add, signs fixed per lane and step).
+    constexpr int LB = R == 32 ? 5 : R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    const int lane_r = lane & (R - 1);
+    const float lf0 = (float)lane_r;
+    float sgn[LB];  // +-2^i: + if bit i of lane' is 0 (flipping it on moves the line up)
 #pragma unroll
-    for (int s = 0; s < R; ++s) {
-        const int l = (lane + s) & (R - 1);
-        lfs[s] = (float)l;
-        lofs[s] = (unsigned)(((kPadL - 3) * kColF + l * BB) * sizeof(float));
-    }
+    for (int i = 0; i < LB; ++i) sgn[i] = ((lane_r >> i) & 1) ? -(float)(1 << i) : (float)(1 << i);
+    // byte offset of line lane' in a staged pixel column, plus the pad shift (3 pad columns,
+    // see the clamp below); bits 0..6, the buffer bases are 128-byte aligned
+    const unsigned lofs0 = (unsigned)(((kPadL - 3) * kColF + lane_r * BB) * sizeof(float));
     const unsigned smem_b = smem_u32(smem);
     const unsigned cmax = (unsigned)(n + 3);
 
@@ -465,34 +486,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const float ab = ang.x, plf = ang.z, c2 = ang.w;
                 const float c1 = fmaf(2.f, ab, -1.f);
                 const float fs = frac - ang.y;
-                const int base4 = base + 4;
+                // candidate_0 + 3 = base + 4 + floor(e); floor(e) is taken as an exact fp32
+                // integer and moved to the integer unit by the 1.5 * 2^23 bias (|e| < 2^22)
+                const int base4 = base + 4 - 0x4B400000;
+                float d[LB];
+#pragma unroll
+                for (int b = 0; b < LB; ++b) d[b] = sgn[b] * plf;
+                const unsigned pbase = cur_b + lofs0;  // bits 0..6 = line lane' (+ pad shift)
+                float e = fmaf(lf0, plf, fs);
                 float blk[BB];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) blk[b] = 0.f;
 #pragma unroll
                 for (int st = 0; st < R; ++st) {
+                    const int gc = st ^ (st >> 1);
+                    if (st > 0) {
+                        // the bit gray(st) flips (lowest set bit of st; folds when unrolled)
+                        const int ib = (st & 1) ? 0 : (st & 2) ? 1 : (st & 4) ? 2 : (st & 8) ? 3 : 4;
+                        if (ib >= 3) {  // re-anchor every 8 lines: e exact to one rounding
+                            e = fmaf((float)(lane_r ^ gc), plf, fs);
+                        } else {
+                            e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
+                        }
+                    }
                     // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
                     // phi = e - floor(e) the hat weights of the 3 candidates are
                     //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
-                    const float e = fmaf(lfs[st], plf, fs);
                     const float fl2 = floorf(e);
                     const float phi = e - fl2;
                     // candidate_0 + 3 clamped to [0, n + 3] in one unsigned min (lanes whose
                     // bin misses the line land in the zero pad columns)
-                    const unsigned cu = min((unsigned)(base4 + (int)fl2), cmax);
+                    const unsigned cu =
+                        min((unsigned)(base4 + __float_as_int(fl2 + 12582912.f)), cmax);
                     const float w0 = fmaf(-ab, phi, ab);
                     const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
                     const float w2 = fmaf(ab, phi, c2);
-                    const unsigned pa = cur_b + cu * (unsigned)(kColF * sizeof(float)) + lofs[st];
+                    const unsigned pa = (pbase ^ (unsigned)(gc * BB * sizeof(float))) +
+                                        cu * (unsigned)(kColF * sizeof(float));
                     float v0[BB], v1[BB], v2[BB];
                     lds_px<BB>(pa, v0);
                     lds_px<BB>(pa + kColF * sizeof(float), v1);
-#pragma unroll
-                    for (int b = 0; b < BB; ++b) blk[b] = fmaf(w1, v1[b], fmaf(w0, v0[b], blk[b]));
+                    fma_px<BB>(blk, w0, v0);
+                    fma_px<BB>(blk, w1, v1);
                     if (w2 > 0.f) {
                         lds_px<BB>(pa + 2 * kColF * sizeof(float), v2);
-#pragma unroll
-                        for (int b = 0; b < BB; ++b) blk[b] = fmaf(w2, v2[b], blk[b]);
+                        fma_px<BB>(blk, w2, v2);
                     }
                 }
 #pragma unroll
@@ -712,7 +750,7 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
     const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~14 KB)
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
-    const size_t smem = a.nbuf * stage_b + tab_b;
+    const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
