@@ -12,38 +12,38 @@
 //     position that projects exactly onto the bin centre.
 //   * Input is the packed copy written by k_rotate_pack (rotate.cu): per image group and
 //     class, blocks of R = 32/BB lines stored [pixel][line][image] — 128 contiguous bytes
-//     per pixel — so a whole block is ONE TMA bulk copy (cp.async.bulk + mbarrier,
-//     double-buffered, issued by one thread: no staging instructions, no registers) and one
+//     per pixel — so a whole block is ONE TMA bulk copy (cp.async.bulk + mbarrier, up to
+//     triple-buffered, issued by one thread: no staging instructions, no registers) and one
 //     LDS.BB fetches a candidate pixel of BB images.
 //   * Work unit = (job, group of BB images sharing the sketch, class, group of K angles);
-//     the S CTAs of a thread-block cluster split the unit's lines.  Staged pixels are reused
-//     by all K angles of the unit.  The kernel is persistent: one cluster per S SMs loops
-//     over the non-empty units (class sizes are counted on the device), and the block
-//     stream continues across units, so the next unit's first blocks are in flight while
-//     the current unit's epilogue runs.
-//   * Bank-conflict-free gathers: lane L processes the lines of a block in the skewed
-//     order l = (L + s) mod R.  The lanes of one shared-memory phase (8 lanes for LDS.128,
-//     16 for LDS.64, 32 for LDS.32) then read R distinct line slots, i.e. distinct banks,
-//     whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way conflicts at
-//     every angle with |beta| < 1 because 8 bins span more than 8 pixels).
-//   * 512 threads (128 registers each), one CTA per SM.  Task = (angle, 32 consecutive
-//     bins), lane = bin; the K x chunks tasks are dealt round-robin to the 32 warps (each
+//     staged pixels are reused by all K angles of the unit.  The kernel is persistent (one
+//     CTA per SM) and stream-K scheduled: the U x nblk (unit, line block) work is cut into
+//     equal contiguous ranges, one per CTA, so every SM streams the same number of blocks;
+//     a unit cut by a range boundary is finished by the last of its pieces (see step 4).
+//     The block stream continues across units, so the next unit's first blocks are in
+//     flight while the current unit's epilogue runs.
+//   * Bank-conflict-free gathers: lane L visits the lines of a block in the order
+//     l = L' ^ gray(s) (L' = L mod R).  The lanes of one shared-memory phase (8 lanes for
+//     LDS.128, 16 for LDS.64, 32 for LDS.32) then read R distinct line slots, i.e. distinct
+//     banks, whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way
+//     conflicts at every angle with |beta| < 1 because 8 bins span more than 8 pixels), and
+//     consecutive lines differ in one bit, so the position moves by one add per line.
+//   * 640 threads (96 registers each), one CTA per SM.  Task = (angle, 32 consecutive
+//     bins), lane = bin; the K x chunks tasks are dealt round-robin to the 20 warps (each
 //     warp gets a mix of angles, whose footprints differ); a thread owns up to kMaxT tasks
-//     and keeps BB accumulators per task in registers: K = 16 kMaxT / chunks angles.
+//     and keeps BB accumulators per task in registers: K = 20 kMaxT / chunks angles.
 //   * Decoupled pipeline: no per-block barrier.  The last warp to finish a staged block
 //     (shared-memory counter) refills its buffer with the block nbuf ahead, so warps drift
 //     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
-//   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset < R (split
-//     precision), 3 hat weights, 3 LDS.BB (the third skipped when its weight
-//     is 0), 3*BB FFMA.  The R lines of a block are summed into a partial before it is
-//     added to the running total (two-level summation).  A chunk skips a block none of its
-//     32 bins sees.
-//   * Unit end: per-CTA partial projections -> shared memory -> fixed-rank-order sum across
-//     the cluster through distributed shared memory (deterministic, no atomics) -> p; for
-//     the MC job also r = p - y_S and per-(unit, rank) partial sums of r^2, summed in a
-//     fixed order by the last CTA to finish (completion counter).
-#include <cooperative_groups.h>
-
+//   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset (split precision,
+//     DESIGN.md §5), 3 hat weights, 3 LDS.BB (the third skipped when its weight is 0) issued
+//     one line ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
+//     summed into a partial before it is added to the running total (two-level summation).
+//     A chunk skips a block none of its 32 bins sees.
+//   * Unit end: a whole unit's sums are complete in registers -> p; for the MC job also
+//     r = p - y_S and per-unit partial sums of r^2, summed in a fixed order by the last CTA
+//     to finish (completion counter).  A split unit's pieces go to L2 slots and the last
+//     piece to arrive adds them in CTA order (deterministic, no float atomics).
 #include <cstdlib>
 
 #include "internal.h"
@@ -51,15 +51,14 @@
 namespace skei {
 namespace {
 
-namespace cg = cooperative_groups;
-
-constexpr int kThreads = 512;
+constexpr int kThreads = 640;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
 // 32-bin tasks per thread: accumulators = kMaxT * BB registers of the 64 available
 template <int BB>
-constexpr int max_tasks() { return 6; }
+constexpr int max_tasks() { return 5; }
 constexpr int kKMax = 16;   // angles per CTA
+constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
 constexpr int kPadL = 4;    // zero pixel columns left of the line data
 constexpr int kPadR = 4;    // ... and right of it (candidates reach n + 2)
 constexpr int kColF = 32;   // floats per staged pixel column (R * BB)
@@ -240,19 +239,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
     __shared__ float s_red[kWarps][BB];
     __shared__ bool s_last;
-    __shared__ int s_fin;       // split unit: this cluster sums the pieces (0/1)
+    __shared__ int s_fin;       // split unit: this CTA sums the pieces (0/1)
+    __shared__ int4 s_task[kWarps * kMaxT];  // per task: angle slot, chunk bin, chunk Pj split
+    __shared__ int s_piece[kMaxPieces];      // split unit: piece slot offsets in CTA order
+    __shared__ int s_npc;
+    __shared__ float sPjf[kKMax];            // Pj (fp32)
 
-    cg::cluster_group cluster = cg::this_cluster();
-    const int S = (int)cluster.num_blocks();
-    const int rank = (int)cluster.block_rank();
-    const int cid = blockIdx.x / S, ncl = gridDim.x / S;
+    const int cid = blockIdx.x, ncl = gridDim.x;
     const int n = a.g.n, n_det = a.g.n_det, n_full = a.g.n_full;
     const int K = a.K, nq = a.nq;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int stage_f = (n + kPadL + kPadR) * kColF;
     int4 *btab = reinterpret_cast<int4 *>(smem + a.nbuf * stage_f);  // [K][nb] block table
     const long part_f = (long)K * n_det * BB;
-    float *part = a.scratch + (long)blockIdx.x * part_f;  // this CTA's partials (L2)
 
     // ---- 1. class sizes per image group -> unit table (identical in every CTA)
     for (int q = warp; q < nq; q += kWarps) {
@@ -296,34 +295,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __syncthreads();
     const Units U{s_uoff, s_nrow, s_uoff[nq]};
     const int total_units = a.njobs * U.per_job;
-    // ---- stream-K work split: the work is W = U x nbc cluster-blocks (nbc = ceil(nblk / S)
-    // line blocks per CTA per unit); cluster c takes the contiguous range [w(c), w(c+1)),
-    // w(c) = c W / ncl, so every cluster gets the same number of blocks whatever U is.  A unit
-    // cut by a range boundary is computed in pieces by consecutive clusters: each piece's
-    // (cluster-summed) partial goes to an L2 slot, and the last piece to finish (per-unit
-    // counter) adds the pieces in cluster order and finishes the unit.
-    const int nbc = (a.nblk + S - 1) / S;
+    // ---- stream-K work split: the work is W = U x nblk line blocks; CTA c takes the
+    // contiguous range [w(c), w(c+1)), w(c) = c W / ncl, so every CTA streams the same number
+    // of blocks whatever U is.  A unit cut by a range boundary is computed in pieces by
+    // consecutive CTAs: each piece's partial projection goes to an L2 slot, and the last
+    // piece to finish (per-unit counter) adds the pieces in CTA order and finishes the unit.
+    const int nbc = a.nblk;
     const long W = (long)total_units * nbc;
     auto wstart = [&](int c) -> long { return (long)c * W / ncl; };
     const long w0 = wstart(cid), w1 = wstart(cid + 1);
     const int u_first = (int)(w0 / nbc), u_last = w1 > w0 ? (int)((w1 - 1) / nbc) : u_first - 1;
-    auto cluster_of = [&](long w) -> int {  // the cluster whose range holds cluster-block w
+    auto cta_of = [&](long w) -> int {  // the CTA whose range holds block w
         int c = (int)(w * ncl / W);
         while (c + 1 < ncl && wstart(c + 1) <= w) ++c;
         while (c > 0 && wstart(c) > w) --c;
         return c;
     };
-    float *pieces = a.scratch + (long)gridDim.x * part_f;  // [ncl][2][part_f]
+    float *pieces = a.scratch;  // [ncl][2][part_f]: the pieces of a CTA's first / last unit
 
-    // this CTA's lines and its blocks of unit u: [blk0 + lo, blk0 + hi)
-    const int blk0 = min(a.nblk, rank * nbc), blk1 = min(a.nblk, blk0 + nbc);
-    const int nb = blk1 - blk0;
+    // this CTA's blocks of unit u: [lo, hi)
     auto unit_blocks = [&](int u, int &lo, int &hi) {
         lo = (int)max(w0 - (long)u * nbc, 0L);
         hi = (int)min(w1 - (long)u * nbc, (long)nbc);
-        lo = min(lo, nb);
-        hi = min(hi, nb);
-        if (hi < lo) hi = lo;
     };
     int G = 0;  // this CTA's block stream: its blocks of u_first .. u_last in order
     for (int u = u_first; u <= u_last; ++u) {
@@ -338,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             if (g < hi - lo) {
                 const UnitId d = decode_unit(U, nq, K, u);
                 const FwdJob &jb = d.job ? a.job[1] : a.job[0];
-                return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + blk0 + lo + g) * n * kColF;
+                return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + lo + g) * n * kColF;
             }
             g -= hi - lo;
         }
@@ -358,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     constexpr int LB = R == 32 ? 5 : R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const int lane_r = lane & (R - 1);
     const float lf0 = (float)lane_r;
+    const float lanef = (float)lane;
     float sgn[LB];  // +-2^i: + if bit i of lane' is 0 (flipping it on moves the line up)
 #pragma unroll
     for (int i = 0; i < LB; ++i) sgn[i] = ((lane_r >> i) & 1) ? -(float)(1 << i) : (float)(1 << i);
@@ -367,12 +361,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     const unsigned smem_b = smem_u32(smem);
     const unsigned cmax = (unsigned)(n + 3);
 
+#ifdef SKEI_FWD_STATS
+    long long st_wait = 0, st_epi = 0, st_pro = 0;
+    const long long st_t0 = clock64();
+#endif
     int gbase = 0;  // stream index of the current unit's first block
     for (int u = u_first; u <= u_last; ++u) {
         int ulo, uhi;
         unit_blocks(u, ulo, uhi);
         const int nbu = uhi - ulo;  // this CTA's blocks of the unit
         const bool full_unit = w0 <= (long)u * nbc && (long)(u + 1) * nbc <= w1;
+#ifdef SKEI_FWD_STATS
+        const long long tp0 = clock64();
+#endif
         const UnitId d = decode_unit(U, nq, K, u);
         const FwdJob job = d.job ? a.job[1] : a.job[0];
         const int b0 = d.q * BB;
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 }
                 sP0[lane] = P0;
                 sPj[lane] = Pj;
+                sPjf[lane] = (float)Pj;
                 sPl[lane] = Pl;
                 sAbsB[lane] = (float)ab;
                 sAng[lane] = make_float4((float)ab, (float)(1.0 / ab), (float)Pl,
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         for (int e = threadIdx.x; e < kcnt * nbu; e += kThreads) {
             const int k = e / nbu, i = e - k * nbu;
             const double Pl = sPl[k], Pj = sPj[k];
-            const double A = sP0[k] + (double)((blk0 + ulo + i) * R) * Pl;
+            const double A = sP0[k] + (double)((ulo + i) * R) * Pl;
             const double fA = floor(A);
             const double sec = 1.0 / (double)sAbsB[k];
             const double lmin = fmin(0.0, (R - 1) * Pl), lmax = fmax(0.0, (R - 1) * Pl);
@@ -444,21 +446,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         }
 
         // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps
-        // per task: angle slot tk (< 0: none), first bin of the chunk tc, and j Pj split into
-        // (int jb, fp32 jf) in fp64 (the bin-dependent part of the position)
-        int tk[kMaxT], tc[kMaxT], jb[kMaxT];
-        float jf[kMaxT];
-#pragma unroll
-        for (int t = 0; t < kMaxT; ++t) {
-            const int tau = warp + kWarps * t;
-            tk[t] = tau < ntask ? tau / a.chunks : -1;
-            tc[t] = tau < ntask ? (tau - tk[t] * a.chunks) * 32 : 0;
-            const double J = (double)(tc[t] + lane) * sPj[tk[t] < 0 ? 0 : tk[t]];
-            const double fJ = floor(J);
-            jb[t] = (int)fJ;
-            jf[t] = (float)(J - fJ);
+        // (task tau = warp + kWarps t): angle slot k (< 0: none), first bin of the chunk c0,
+        // and c0 Pj split into (int, fp32 fraction) in fp64; a lane adds its lane Pj in fp32
+        for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads) {
+            int4 td = make_int4(-1, 0, 0, 0);
+            if (tau < ntask) {
+                td.x = tau / a.chunks;
+                td.y = (tau - td.x * a.chunks) * 32;
+                const double J = (double)td.y * sPj[td.x];
+                const double fJ = floor(J);
+                td.z = (int)fJ;
+                td.w = __float_as_int((float)(J - fJ));
+            }
+            s_task[tau] = td;
         }
-        __syncthreads();  // block table complete
+        __syncthreads();  // block table and task table complete
+#ifdef SKEI_FWD_STATS
+        st_pro += clock64() - tp0;
+#endif
         float acc[kMaxT][BB];
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t)
@@ -469,15 +474,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             const int g = gbase + i;
             const int cb = g % nbuf;
             const unsigned cur_b = smem_b + (unsigned)(cb * stage_f * sizeof(float));
+#ifdef SKEI_FWD_STATS
+            const long long tw0 = clock64();
+#endif
             mbar_wait(&full[cb], (unsigned)((g / nbuf) & 1));
+#ifdef SKEI_FWD_STATS
+            st_wait += clock64() - tw0;
+#endif
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
-                const int k = tk[t];
-                if (k < 0) break;  // warp-uniform
+                const int4 td = s_task[warp + kWarps * t];  // warp-uniform (broadcast)
+                const int k = td.x;
+                if (k < 0) break;
                 const int4 ent = btab[k * nbu + i];
-                if (tc[t] > ent.w || tc[t] + 31 < ent.z) continue;  // chunk misses the block
-                int base = ent.x + jb[t];
-                float frac = __int_as_float(ent.y) + jf[t];
+                if (td.y > ent.w || td.y + 31 < ent.z) continue;  // chunk misses the block
+                int base = ent.x + td.z;
+                float frac = __int_as_float(ent.y) + __int_as_float(td.w);
                 if (frac >= 1.f) {
                     frac -= 1.f;
                     base += 1;
@@ -485,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const float4 ang = sAng[k];  // |beta|, 1/|beta|, Pl, 2 - 3|beta|
                 const float ab = ang.x, plf = ang.z, c2 = ang.w;
                 const float c1 = fmaf(2.f, ab, -1.f);
-                const float fs = frac - ang.y;
+                // + lane Pj (< 32 * sqrt 2, fp32): the lane's bin within the chunk
+                const float fs = fmaf(lanef, sPjf[k], frac - ang.y);
                 // candidate_0 + 3 = base + 4 + floor(e); floor(e) is taken as an exact fp32
                 // integer and moved to the integer unit by the 1.5 * 2^23 bias (|e| < 2^22)
                 const int base4 = base + 4 - 0x4B400000;
@@ -497,41 +510,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 float blk[BB];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) blk[b] = 0.f;
-#pragma unroll
-                for (int st = 0; st < R; ++st) {
+                // one line: e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and
+                // with phi = e - floor(e) the hat weights of the 3 candidates are
+                //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi;
+                // the 2-3 candidate pixels are loaded one line ahead of their use
+                float v[2][3][BB], w[2][3];
+                auto load_line = [&](int st, float (&vv)[3][BB], float (&ww)[3]) {
                     const int gc = st ^ (st >> 1);
-                    if (st > 0) {
-                        // the bit gray(st) flips (lowest set bit of st; folds when unrolled)
-                        const int ib = (st & 1) ? 0 : (st & 2) ? 1 : (st & 4) ? 2 : (st & 8) ? 3 : 4;
-                        if (ib >= 3) {  // re-anchor every 8 lines: e exact to one rounding
-                            e = fmaf((float)(lane_r ^ gc), plf, fs);
-                        } else {
-                            e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
-                        }
-                    }
-                    // e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and with
-                    // phi = e - floor(e) the hat weights of the 3 candidates are
-                    //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi
                     const float fl2 = floorf(e);
                     const float phi = e - fl2;
                     // candidate_0 + 3 clamped to [0, n + 3] in one unsigned min (lanes whose
                     // bin misses the line land in the zero pad columns)
                     const unsigned cu =
                         min((unsigned)(base4 + __float_as_int(fl2 + 12582912.f)), cmax);
-                    const float w0 = fmaf(-ab, phi, ab);
-                    const float w1 = 1.f - fabsf(fmaf(-ab, phi, c1));
-                    const float w2 = fmaf(ab, phi, c2);
+                    ww[0] = fmaf(-ab, phi, ab);
+                    ww[1] = 1.f - fabsf(fmaf(-ab, phi, c1));
+                    ww[2] = fmaf(ab, phi, c2);
                     const unsigned pa = (pbase ^ (unsigned)(gc * BB * sizeof(float))) +
                                         cu * (unsigned)(kColF * sizeof(float));
-                    float v0[BB], v1[BB], v2[BB];
-                    lds_px<BB>(pa, v0);
-                    lds_px<BB>(pa + kColF * sizeof(float), v1);
-                    fma_px<BB>(blk, w0, v0);
-                    fma_px<BB>(blk, w1, v1);
-                    if (w2 > 0.f) {
-                        lds_px<BB>(pa + 2 * kColF * sizeof(float), v2);
-                        fma_px<BB>(blk, w2, v2);
+                    lds_px<BB>(pa, vv[0]);
+                    lds_px<BB>(pa + kColF * sizeof(float), vv[1]);
+                    if (ww[2] > 0.f) lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
+                };
+                load_line(0, v[0], w[0]);
+#pragma unroll
+                for (int st = 0; st < R; ++st) {
+                    const int cur = st & 1;
+                    if (st + 1 < R) {
+                        const int sn = st + 1, gc = sn ^ (sn >> 1);
+                        // the bit gray(sn) flips (lowest set bit of sn; folds when unrolled)
+                        const int ib = (sn & 1) ? 0 : (sn & 2) ? 1 : (sn & 4) ? 2 : (sn & 8) ? 3 : 4;
+                        if (ib >= 3) {  // re-anchor every 8 lines: e exact to one rounding
+                            e = fmaf((float)(lane_r ^ gc), plf, fs);
+                        } else {
+                            e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
+                        }
+                        load_line(sn, v[cur ^ 1], w[cur ^ 1]);
                     }
+                    fma_px<BB>(blk, w[cur][0], v[cur][0]);
+                    fma_px<BB>(blk, w[cur][1], v[cur][1]);
+                    if (w[cur][2] > 0.f) fma_px<BB>(blk, w[cur][2], v[cur][2]);
                 }
 #pragma unroll
                 for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
@@ -549,102 +567,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             }
         }
 
-        // ---- 4. unit epilogue: partials -> shared memory [kcnt][n_det][BB], then the
-        // fixed-rank-order cluster sum (DSMEM) -> p, and the fused MC residual for job 0
-#pragma unroll
-        for (int t = 0; t < kMaxT; ++t) {
-            const int k = tk[t];
-            if (k < 0) break;
-            const int j = tc[t] + lane;
-            if (j < n_det) {
-#pragma unroll
-                for (int b = 0; b < BB; ++b) part[((long)k * n_det + j) * BB + b] = acc[t][b];
-            }
-        }
+#ifdef SKEI_FWD_STATS
+        const long long te0 = clock64();
+#endif
+        // ---- 4. unit epilogue.  A whole unit is complete in this CTA's registers: each lane
+        // writes its (angle, bin) sums to p and, for the MC job, r = p - y_S and sum r^2.  A
+        // split unit's piece goes to this CTA's L2 slot; the last piece to arrive (counter)
+        // adds the pieces in CTA order and finishes the unit.
         gbase += nbu;
-        cluster.sync();  // partials of every rank written (cluster scope release/acquire)
-        const float *cpart = a.scratch + (long)(blockIdx.x - rank) * part_f;  // rank 0's
-        // this rank's slice of the unit's (angle, bin) pairs; the S partials of a pair are one
-        // BB-vector each, summed in rank order
-        const int T2 = kcnt * n_det;
-        const int per2 = (T2 + S - 1) / S;
-        const int p0 = min(T2, rank * per2), p1 = min(T2, p0 + per2);
-        auto cluster_sum = [&](int o2, float (&sv)[BB]) {
-            float v[BB];
-            ldcg_vec<BB>(cpart + (long)o2 * BB, sv);
-            for (int q = 1; q < S; ++q) {
-                ldcg_vec<BB>(cpart + q * part_f + (long)o2 * BB, v);
-#pragma unroll
-                for (int b = 0; b < BB; ++b) sv[b] += v[b];
-            }
-        };
-        bool finish = full_unit;
-        const float *pc_first = nullptr;  // split unit: pieces of clusters c0 .. c1
-        int c0 = 0, c1 = -1;
-        if (!full_unit) {
-            // this cluster's piece -> its slot (0 if u is the cluster's first unit, else 1)
-            float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
-            for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
-                float sv[BB];
-                cluster_sum(o2, sv);
-                stg_vec<BB>(mine + (long)o2 * BB, sv);
-            }
-            __threadfence();
-            c0 = cluster_of((long)u * nbc);
-            c1 = cluster_of((long)u * nbc + nbc - 1);
-            int npc = 0;  // pieces = non-empty clusters c0 .. c1
-            for (int c = c0; c <= c1; ++c) npc += wstart(c + 1) > wstart(c);
-            cluster.sync();  // the whole piece written (and fenced) by every rank
-            if (rank == 0 && threadIdx.x == 0)
-                s_fin = atomicAdd(a.queue + c0, 1u) == (unsigned)(npc - 1) ? 1 : 0;
-            cluster.sync();
-            finish = cluster.map_shared_rank(&s_fin, 0)[0] != 0;
-            if (finish) {
-                __threadfence();
-                pc_first = pieces;
-            }
-        }
         const long img_stride = (long)a.m * n_det;
         const bool mc = job.y != nullptr;
         float racc[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) racc[b] = 0.f;
-        if (finish) {
-            for (int o2 = p0 + threadIdx.x; o2 < p1; o2 += kThreads) {
-                const int k = o2 / n_det;
-                const int j = o2 - k * n_det;
-                const int slot = sSlot[k];
-                float sv[BB];
-                if (full_unit) {
-                    cluster_sum(o2, sv);
-                } else {  // the pieces of clusters c0 .. c1, in cluster order
+        auto finish_pair = [&](int slot, int j, const float (&sv)[BB]) {
+            const long pj = (long)slot * n_det + j;
 #pragma unroll
-                    for (int b = 0; b < BB; ++b) sv[b] = 0.f;
-                    for (int c = c0; c <= c1; ++c) {
-                        if (wstart(c + 1) == wstart(c)) continue;  // empty range
-                        const int cslot = u == (int)(wstart(c) / nbc) ? 0 : 1;  // u first of c?
+            for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
+            if (mc) {
+                const long yj = (long)idx[slot] * n_det + j;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) {
+                    const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
+                    if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
+                    racc[b] = fmaf(dr, dr, racc[b]);
+                }
+            }
+        };
+        bool finish = full_unit;
+        if (full_unit) {
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t) {
+                const int4 td = s_task[warp + kWarps * t];
+                if (td.x < 0) break;
+                const int j = td.y + lane;
+                if (j < n_det) finish_pair(sSlot[td.x], j, acc[t]);
+            }
+        } else {
+            float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t) {
+                const int4 td = s_task[warp + kWarps * t];
+                if (td.x < 0) break;
+                const int j = td.y + lane;
+                if (j < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j) * BB, acc[t]);
+            }
+            __threadfence();
+            __syncthreads();  // the whole piece written (and fenced)
+            if (threadIdx.x == 0) {
+                // the pieces: non-empty CTA ranges c0 .. c1, slot 0 if u is the CTA's first unit
+                const int c0 = cta_of((long)u * nbc), c1 = cta_of((long)u * nbc + nbc - 1);
+                int npc = 0;
+                for (int c = c0; c <= c1; ++c) {
+                    const long ws = wstart(c);
+                    if (wstart(c + 1) == ws) continue;
+                    s_piece[npc++] = c * 2 + (u == (int)(ws / nbc) ? 0 : 1);
+                }
+                s_npc = npc;
+                const bool last = atomicAdd(a.queue + c0, 1u) == (unsigned)(npc - 1);
+                if (last) a.queue[c0] = 0u;  // ready for the next launch
+                s_fin = last ? 1 : 0;
+            }
+            __syncthreads();
+            finish = s_fin != 0;
+            if (finish) {
+                __threadfence();
+                const int npc = s_npc;
+                for (int o2 = threadIdx.x; o2 < kcnt * n_det; o2 += kThreads) {
+                    const int k = o2 / n_det;
+                    float sv[BB];
+                    ldcg_vec<BB>(pieces + (long)s_piece[0] * part_f + (long)o2 * BB, sv);
+                    for (int c = 1; c < npc; ++c) {  // the pieces in CTA order
                         float v[BB];
-                        ldcg_vec<BB>(pc_first + ((long)c * 2 + cslot) * part_f + (long)o2 * BB, v);
+                        ldcg_vec<BB>(pieces + (long)s_piece[c] * part_f + (long)o2 * BB, v);
 #pragma unroll
                         for (int b = 0; b < BB; ++b) sv[b] += v[b];
                     }
-                }
-                const long pj = (long)slot * n_det + j;
-#pragma unroll
-                for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
-                if (mc) {
-                    const long yj = (long)idx[slot] * n_det + j;
-#pragma unroll
-                    for (int b = 0; b < BB; ++b) {
-                        const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
-                        if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
-                        racc[b] = fmaf(dr, dr, racc[b]);
-                    }
+                    finish_pair(sSlot[k], o2 - k * n_det, sv);
                 }
             }
-            if (!full_unit && rank == 0 && threadIdx.x == 0) a.queue[c0] = 0u;  // next launch
         }
-        if (mc && finish) {  // per-(unit, rank) partial of each image of the group
+        if (mc && finish) {  // per-unit partial of each image of the group
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
                 float v = racc[b];
@@ -653,15 +656,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (lane == 0) s_red[warp][b] = v;
             }
         }
-        cluster.sync();  // partials consumed; s_red complete
+        __syncthreads();  // s_red complete; s_task / sSlot free for the next unit
         if (mc && finish && threadIdx.x < BB) {
             float v = 0.f;
             for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
-            const int slot = (u - U.uoff[d.q]) * S + rank;
-            a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + slot] = v;
+            a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
         }
+#ifdef SKEI_FWD_STATS
+        st_epi += clock64() - te0;
+#endif
     }
 
+#ifdef SKEI_FWD_STATS
+    if (lane == 0 && (blockIdx.x % 37) == 0)
+        printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld\n",
+               blockIdx.x, warp, u_last - u_first + 1, G, st_wait, st_pro, st_epi, clock64() - st_t0);
+#endif
     // ---- 5. MC residual final: the last CTA sums each image's (unit, rank) partials in order
     if (!a.job[0].y) return;
     __threadfence();
@@ -672,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __threadfence();
     for (int b = warp; b < a.B; b += kWarps) {
         const int q = b / BB;
-        const int ns = (U.uoff[q + 1] - U.uoff[q]) * S;
+        const int ns = U.uoff[q + 1] - U.uoff[q];
         double sum = 0.0;
         for (int i = lane; i < ns; i += 32) sum += (double)__ldcg(a.mc_part + (long)b * a.mc_slots + i);
 #pragma unroll
@@ -680,61 +690,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         if (lane == 0) a.mc_out[b] = (float)sum;
     }
     if (threadIdx.x == 0) *a.mc_ctr = 0u;  // ready for the next launch
-}
-
-// Co-resident clusters of size S for this kernel configuration (cached): a persistent grid
-// must not exceed it, or the surplus clusters run as a second round.
-template <int BB>
-int max_clusters(int S, size_t smem, int num_sms) {
-    static int cache[9] = {0};
-    static size_t cache_smem[9] = {0};
-    if (cache[S] > 0 && cache_smem[S] == smem) return cache[S];
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((num_sms / S) * S), 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)S;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, k_radon_fwd<BB>, &cfg) != cudaSuccess || ncl < 1) {
-        cudaGetLastError();
-        ncl = num_sms / S;
-    }
-    cache[S] = ncl;
-    cache_smem[S] = smem;
-    return ncl;
-}
-
-// Cluster size S (line split) of the persistent grid: ncl(S) co-resident clusters share
-// `units`, each costing ceil(nblk / S) + 1 blocks per CTA (the +1 is the unit's
-// prologue/epilogue); stream-K splits the blocks evenly, so the makespan is about
-// units (ceil(nblk / S) + 1) / ncl blocks plus one split-unit epilogue.  SKEI_FWD_CLUSTER=S overrides the choice (tuning/diagnostics).
-template <int BB>
-int pick_cluster(long units, int nblk, int num_sms, size_t smem, int *ncl_out) {
-    static int forced = -1;
-    if (forced < 0) {
-        const char *e = getenv("SKEI_FWD_CLUSTER");
-        forced = e ? atoi(e) : 0;
-        if (forced < 0 || forced > 8) forced = 0;
-    }
-    int best = 4, best_ncl = 1;
-    double best_cost = 1e30;
-    for (int S = 1; S <= 8; ++S) {
-        const int ncl = max_clusters<BB>(S, smem, num_sms);
-        const double cost = (double)units * ((nblk + S - 1) / S + 1.0) / ncl + 1.0;
-        if ((forced && S == forced) || (!forced && cost < best_cost - 1e-9)) {
-            best_cost = cost;
-            best = S;
-            best_ncl = ncl;
-        }
-    }
-    *ncl_out = best_ncl;
-    return best;
 }
 
 template <int BB>
@@ -748,28 +703,23 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
-    const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~14 KB)
+    const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~11 KB)
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
     const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const long units = (long)a.njobs * a.nq * ((a.m + a.K - 1) / a.K + 1);
-    int ncl = 1;
-    const int S = pick_cluster<BB>(units, a.nblk, num_sms, smem, &ncl);
+    // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared memory)
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB>, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(ncl * S), 1, 1);
+    cfg.gridDim = dim3((unsigned)(num_sms * per_sm), 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)S;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, k_radon_fwd<BB>, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
@@ -778,9 +728,9 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
 }  // namespace
 
 size_t fwd_scratch_floats(const skei_plan *plan) {
-    // grid <= num_sms CTAs, each K * n_det * BB <= kWarps * kMaxT * 32 * 4 floats, then two
-    // split-unit piece slots per cluster (<= num_sms clusters)
-    return (size_t)3 * plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
+    // two split-unit piece slots per CTA (grid <= num_sms), each K * n_det * BB <=
+    // kWarps * kMaxT * 32 * 4 floats
+    return (size_t)2 * plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
 }
 
 size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
@@ -790,7 +740,7 @@ size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
     int K = (kWarps * max_tasks<1>()) / chunks;  // the smallest K over the image groups
     if (K > kKMax) K = kKMax;
     if (K < 1) K = 1;
-    return (size_t)8 * ((m + K - 1) / K + 2);  // cluster size x units per image group
+    return (size_t)((m + K - 1) / K + 2);  // units per image group
 }
 
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
