@@ -51,13 +51,17 @@
 namespace skei {
 namespace {
 
-constexpr int kThreads = 640;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
-// 32-bin tasks per thread: accumulators = kMaxT * BB registers of the 64 available
+// 32-bin task slots per warp (each lane: kMaxT * BB accumulator registers)
 template <int BB>
-constexpr int max_tasks() { return 5; }
+constexpr int max_tasks() { return 8; }
 constexpr int kKMax = 16;   // angles per CTA
+#ifndef SKEI_FWD_AHEAD
+#define SKEI_FWD_AHEAD 2
+#endif
+constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ahead of use
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
 constexpr int kPadL = 4;    // zero pixel columns left of the line data
 constexpr int kPadR = 4;    // ... and right of it (candidates reach n + 2)
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int s_fin;       // split unit: this CTA sums the pieces (0/1)
     __shared__ int4 s_task[kWarps * kMaxT];  // per task: angle slot, chunk bin, chunk Pj split
     __shared__ int s_piece[kMaxPieces];      // split unit: piece slot offsets in CTA order
+    __shared__ int s_cost[kWarps * kMaxT];   // per task: blocks its chunk touches
     __shared__ int s_npc;
     __shared__ float sPjf[kKMax];            // Pj (fp32)
 
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     const unsigned cmax = (unsigned)(n + 3);
 
 #ifdef SKEI_FWD_STATS
-    long long st_wait = 0, st_epi = 0, st_pro = 0;
+    long long st_wait = 0, st_epi = 0, st_pro = 0, st_active = 0, st_lanes = 0;
     const long long st_t0 = clock64();
 #endif
     int gbase = 0;  // stream index of the current unit's first block
@@ -421,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                                          (float)(2.0 - 3.0 * ab));
             }
         }
+        for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads) s_cost[tau] = 0;
         __syncthreads();
         const int kcnt = sCount;
         const int ntask = kcnt * a.chunks;
@@ -443,22 +449,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             ent.z = (int)jl;
             ent.w = (int)jh;
             btab[e] = ent;
+            // the chunks c with 32 c <= jh and 32 c + 31 >= jl touch this block
+            const int clo = ent.z <= 0 ? 0 : ent.z / 32;
+            const int chi = ent.w < 0 ? -1 : min(a.chunks - 1, ent.w / 32);
+            for (int c = clo; c <= chi; ++c) atomicAdd(&s_cost[k * a.chunks + c], 1);
         }
 
-        // ---- 3. tasks: (angle k, 32-bin chunk) pairs dealt round-robin to the warps
-        // (task tau = warp + kWarps t): angle slot k (< 0: none), first bin of the chunk c0,
-        // and c0 Pj split into (int, fp32 fraction) in fp64; a lane adds its lane Pj in fp32
-        for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads) {
-            int4 td = make_int4(-1, 0, 0, 0);
-            if (tau < ntask) {
-                td.x = tau / a.chunks;
-                td.y = (tau - td.x * a.chunks) * 32;
-                const double J = (double)td.y * sPj[td.x];
-                const double fJ = floor(J);
-                td.z = (int)fJ;
-                td.w = __float_as_int((float)(J - fJ));
+        // ---- 3. tasks: (angle k, 32-bin chunk) pairs.  A warp runs a task's whole line loop
+        // on every block its chunk touches, so a task costs the number of such blocks
+        // (counted while the block table is built); chunks that touch no block are dropped.
+        // The others are ranked by cost (descending, ties by index) and dealt to the warps
+        // in snake order (rank r -> round r / kWarps, warp r mod kWarps, reversed on odd
+        // rounds), which balances the warps to within about one task.  Per task: angle slot
+        // k (< 0: none), first bin of the chunk c0, and c0 Pj split into (int, fp32
+        // fraction) in fp64; a lane adds its lane Pj in fp32.
+        __syncthreads();  // block table and task costs complete
+        for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads)
+            s_task[tau] = make_int4(-1, 0, 0, 0);
+        __syncthreads();
+        for (int tau = threadIdx.x; tau < ntask; tau += kThreads) {
+            const int cst = s_cost[tau];
+            if (cst == 0) continue;
+            int r = 0;
+            for (int o = 0; o < ntask; ++o) {
+                const int co = s_cost[o];
+                r += (co > cst) || (co == cst && o < tau);
             }
-            s_task[tau] = td;
+            const int round = r / kWarps, wi = r - round * kWarps;
+            const int w = (round & 1) ? kWarps - 1 - wi : wi;
+            int4 td;
+            td.x = tau / a.chunks;
+            td.y = (tau - td.x * a.chunks) * 32;
+            const double J = (double)td.y * sPj[td.x];
+            const double fJ = floor(J);
+            td.z = (int)fJ;
+            td.w = __float_as_int((float)(J - fJ));
+            s_task[w + kWarps * round] = td;
         }
         __syncthreads();  // block table and task table complete
 #ifdef SKEI_FWD_STATS
@@ -488,6 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (k < 0) break;
                 const int4 ent = btab[k * nbu + i];
                 if (td.y > ent.w || td.y + 31 < ent.z) continue;  // chunk misses the block
+#ifdef SKEI_FWD_STATS
+                ++st_active;
+                st_lanes += max(0, min(td.y + 31, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
+#endif
                 int base = ent.x + td.z;
                 float frac = __int_as_float(ent.y) + __int_as_float(td.w);
                 if (frac >= 1.f) {
@@ -513,8 +543,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 // one line: e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and
                 // with phi = e - floor(e) the hat weights of the 3 candidates are
                 //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi;
-                // the 2-3 candidate pixels are loaded one line ahead of their use
-                float v[2][3][BB], w[2][3];
+                // the 2-3 candidate pixels are loaded kAhead lines ahead of their use
+                constexpr int D = kAhead < R ? kAhead : R - 1;  // lines in flight ahead of use
+                float v[D + 1][3][BB], w[D + 1][3];
                 auto load_line = [&](int st, float (&vv)[3][BB], float (&ww)[3]) {
                     const int gc = st ^ (st >> 1);
                     const float fl2 = floorf(e);
@@ -532,20 +563,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     lds_px<BB>(pa + kColF * sizeof(float), vv[1]);
                     if (ww[2] > 0.f) lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
                 };
-                load_line(0, v[0], w[0]);
+                // e of line gray(sn) from that of line gray(sn - 1)
+                auto advance = [&](int sn) {
+                    const int gc = sn ^ (sn >> 1);
+                    // the bit gray(sn) flips (lowest set bit of sn; folds when unrolled)
+                    const int ib = (sn & 1) ? 0 : (sn & 2) ? 1 : (sn & 4) ? 2 : (sn & 8) ? 3 : 4;
+                    if (ib >= 3) {  // re-anchor every 8 lines: e exact to one rounding
+                        e = fmaf((float)(lane_r ^ gc), plf, fs);
+                    } else {
+                        e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
+                    }
+                };
+#pragma unroll
+                for (int st = 0; st < D; ++st) {
+                    if (st > 0) advance(st);
+                    load_line(st, v[st], w[st]);
+                }
 #pragma unroll
                 for (int st = 0; st < R; ++st) {
-                    const int cur = st & 1;
-                    if (st + 1 < R) {
-                        const int sn = st + 1, gc = sn ^ (sn >> 1);
-                        // the bit gray(sn) flips (lowest set bit of sn; folds when unrolled)
-                        const int ib = (sn & 1) ? 0 : (sn & 2) ? 1 : (sn & 4) ? 2 : (sn & 8) ? 3 : 4;
-                        if (ib >= 3) {  // re-anchor every 8 lines: e exact to one rounding
-                            e = fmaf((float)(lane_r ^ gc), plf, fs);
-                        } else {
-                            e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
-                        }
-                        load_line(sn, v[cur ^ 1], w[cur ^ 1]);
+                    const int cur = st % (D + 1);
+                    if (st + D < R) {
+                        advance(st + D);
+                        load_line(st + D, v[(st + D) % (D + 1)], w[(st + D) % (D + 1)]);
                     }
                     fma_px<BB>(blk, w[cur][0], v[cur][0]);
                     fma_px<BB>(blk, w[cur][1], v[cur][1]);
@@ -595,6 +634,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             }
         };
         bool finish = full_unit;
+        // chunks that touch no block of the unit (dropped tasks) sum to zero
+        float zero[BB];
+#pragma unroll
+        for (int b = 0; b < BB; ++b) zero[b] = 0.f;
         if (full_unit) {
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
@@ -602,6 +645,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (td.x < 0) break;
                 const int j = td.y + lane;
                 if (j < n_det) finish_pair(sSlot[td.x], j, acc[t]);
+            }
+            for (int tau = warp; tau < ntask; tau += kWarps) {
+                if (s_cost[tau] != 0) continue;
+                const int k = tau / a.chunks, j = (tau - k * a.chunks) * 32 + lane;
+                if (j < n_det) finish_pair(sSlot[k], j, zero);
             }
         } else {
             float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
@@ -611,6 +659,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (td.x < 0) break;
                 const int j = td.y + lane;
                 if (j < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j) * BB, acc[t]);
+            }
+            for (int tau = warp; tau < ntask; tau += kWarps) {
+                if (s_cost[tau] != 0) continue;
+                const int k = tau / a.chunks, j = (tau - k * a.chunks) * 32 + lane;
+                if (j < n_det) stg_vec<BB>(mine + ((long)k * n_det + j) * BB, zero);
             }
             __threadfence();
             __syncthreads();  // the whole piece written (and fenced)
@@ -669,8 +722,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 
 #ifdef SKEI_FWD_STATS
     if (lane == 0 && (blockIdx.x % 37) == 0)
-        printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld\n",
-               blockIdx.x, warp, u_last - u_first + 1, G, st_wait, st_pro, st_epi, clock64() - st_t0);
+        printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld active %lld "
+               "lanes %lld\n", blockIdx.x, warp, u_last - u_first + 1, G, st_wait, st_pro, st_epi,
+               clock64() - st_t0, st_active, st_lanes);
 #endif
     // ---- 5. MC residual final: the last CTA sums each image's (unit, rank) partials in order
     if (!a.job[0].y) return;

@@ -38,7 +38,8 @@ def main():
     for w in sorted(seen):
         r = seen[w]
         print(f"cta {r[0]} warp {w:2d} units {r[2]} blocks {r[3]} wait {r[4]:7d} pro {r[5]:6d} "
-              f"epi {r[6]:6d} compute {r[7] - r[4] - r[5] - r[6]:7d} total {r[7]}")
+              f"epi {r[6]:6d} compute {r[7] - r[4] - r[5] - r[6]:7d} total {r[7]} "
+              f"active tasks {r[8]} lanes/task {r[9] / max(1, r[8]):.1f}")
 
 
 if __name__ == "__main__":
