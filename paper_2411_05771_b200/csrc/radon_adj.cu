@@ -69,6 +69,27 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// acc += w0 q0 + w1 q1 + w2 q2 over BB images (in that order), as packed fp32x2 FMAs
+// (bitwise the same as the scalar fmaf chain)
+template <int BB>
+__device__ __forceinline__ void tap3(float (&acc)[BB], float w0, float w1, float w2,
+                                     const float (&q0)[BB], const float (&q1)[BB],
+                                     const float (&q2)[BB]) {
+    if constexpr (BB == 1) {
+        acc[0] = fmaf(w2, q2[0], fmaf(w1, q1[0], fmaf(w0, q0[0], acc[0])));
+    } else {
+#pragma unroll
+        for (int b = 0; b < BB; b += 2) {
+            float2 r = make_float2(acc[b], acc[b + 1]);
+            r = __ffma2_rn(make_float2(w0, w0), make_float2(q0[b], q0[b + 1]), r);
+            r = __ffma2_rn(make_float2(w1, w1), make_float2(q1[b], q1[b + 1]), r);
+            r = __ffma2_rn(make_float2(w2, w2), make_float2(q2[b], q2[b + 1]), r);
+            acc[b] = r.x;
+            acc[b + 1] = r.y;
+        }
+    }
+}
+
 // hat weights of a position u in [0, 2] against bins 0, 1, 2
 __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
     w0 = fmaxf(0.f, 1.f - u);
@@ -180,13 +201,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
                     load_bins<BB>(wt, q0);
                     load_bins<BB>(wt + BB, q1);
                     load_bins<BB>(wt + 2 * BB, q2);
-#pragma unroll
-                    for (int b = 0; b < BB; ++b) {
-                        acc[jj][p][0][b] =
-                            fmaf(w12, q2[b], fmaf(w11, q1[b], fmaf(w10, q0[b], acc[jj][p][0][b])));
-                        acc[jj][p][1][b] =
-                            fmaf(w22, q2[b], fmaf(w21, q1[b], fmaf(w20, q0[b], acc[jj][p][1][b])));
-                    }
+                    tap3<BB>(acc[jj][p][0], w10, w11, w12, q0, q1, q2);
+                    tap3<BB>(acc[jj][p][1], w20, w21, w22, q0, q1, q2);
                 }
             }
         }
