@@ -54,7 +54,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // Workspace: [q: B*m*n_det floats][residual partials][4 packed images: x1 rows/cols, x2
 // rows/cols, each pack_floats() for the largest image group]
 struct WsLayout {
-    size_t q, res, pack[4], ctr, mcpart, eipart, fscr, total;
+    size_t q, res, pack[4], ctr, mcpart, eipart, fscr, qi, ri, total;
 };
 WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     WsLayout w;
@@ -78,8 +78,12 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     off += align256(sizeof(float) * (size_t)B * fwd_mc_slots(plan, B, m, 0));
     w.eipart = off;
     off += align256(sizeof(float) * adj_ei_part_floats(plan, B));
-    w.fscr = off;  // forward per-CTA partials
+    w.fscr = off;  // forward split-unit pieces
     off += align256(sizeof(float) * fwd_scratch_floats(plan));
+    w.qi = off;  // interleaved padded q and r for the backprojector's bulk copies
+    off += align256(sizeof(float) * adj_il_floats(plan, B, m));
+    w.ri = off;
+    off += align256(sizeof(float) * adj_il_floats(plan, B, m));
     w.total = off;
     return w;
 }
@@ -394,18 +398,22 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     SKEI_CUDA(mark(1));
     // a3 + a7 (MC part): p1 = A_S x1 with r = p1 - y_S and mc = ||r||^2 fused into its
     // epilogue, and p2 = A_S x2, in one launch
+    // with image groups of 4, q and r are also written in the backprojector's interleaved
+    // padded layout (its windows are then one bulk copy per angle)
+    const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
+    float *qi = il ? ws_f(ws, wl.qi) : nullptr, *ri = il ? ws_f(ws, wl.ri) : nullptr;
     FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1, y, o->r},
                     {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
     FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr));
     SKEI_CUDA(mark(2));
-    // a4: q = ramp(p2)
-    SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s));
+    // a4: q = ramp(p2); the same launch also copies r into the interleaved layout
+    SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s, qi, m, 4, o->r, ri));
     SKEI_CUDA(mark(3));
     // a5 + a8 (+ a7 EI part when x3 is the identity network's x_fbp): x_fbp = (pi/2m) A_S^T q
     // and grad = 2 A_S^T r in one launch, ei = ||x2 - x_fbp||^2 fused into its epilogue
-    AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale}, {o->r, o->grad, 2.0f}};
+    AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale, qi}, {o->r, o->grad, 2.0f, ri}};
     AdjEi eif{o->x2, ws_f(ws, wl.eipart), ctr + 1, o->ei};
     SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, x3_in ? nullptr : &eif));
     SKEI_CUDA(mark(4));

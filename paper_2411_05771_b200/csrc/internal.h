@@ -94,7 +94,15 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
 
 // Backprojection; up to two jobs sharing one angle list (FBP of q and gradient of r).
 // Job 0 may fuse ei = sum (x2 - x_job0)^2 (identity network): partial sums per tile.
-struct AdjJob { const float *p; float *x; float scale; };
+// Interleaved padded sinogram for the backprojector's bulk window copies: row (b, k) ->
+// [b / 4][k][kAdjPad + j][b % 4], rows of n_det + 2 kAdjPad bins, the pads zero, so one
+// angle's detector window of a tile is one contiguous, in-bounds 16-byte-aligned copy.
+constexpr int kAdjPad = 48;
+inline size_t adj_il_floats(const skei_plan *plan, int B, int m) {
+    return (size_t)((B + 3) / 4) * m * (plan->n_det + 2 * kAdjPad) * 4;
+}
+// pi: the same sinogram as p in the interleaved layout (or NULL: staged from p)
+struct AdjJob { const float *p; float *x; float scale; const float *pi = nullptr; };
 struct AdjEi {
     const float *x2;  // [B][n][n]
     float *part;      // [B][adj_ei_part_floats / B]
@@ -108,7 +116,8 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
-                        cudaStream_t s);
+                        cudaStream_t s, float *qi = nullptr, int m = 0, int bb = 0,
+                        const float *rs = nullptr, float *ri = nullptr);
 
 // Residual: partials in ws (float2 per (image, chunk)), then final reduce.
 size_t residual_ws_bytes(const skei_plan *plan, int B, int m);

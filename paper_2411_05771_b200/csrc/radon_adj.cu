@@ -23,6 +23,7 @@
 //     sum (x2 - x_fbp)^2 per tile and image, reduced in fixed order by the last CTA.
 // Work per (pixel, angle, image) = 2 taps; per pixel pair and angle 3 LDS.BB per job.
 #include "internal.h"
+#include "tma.h"
 
 namespace skei {
 namespace {
@@ -97,13 +98,16 @@ __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
     w2 = fmaxf(0.f, u - 1.f);
 }
 
-template <int BB, int NJ>
+// ILM: bit jj set = job jj's windows are bulk copies from its interleaved padded sinogram
+template <int BB, int NJ, int ILM>
 __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
-    __shared__ __align__(16) float win[2][NJ][kKC * kW * BB];
+    __shared__ __align__(128) float win[2][NJ][kKC * kW * BB];
     __shared__ float s_off[2][kKC], s_cos[2][kKC], s_sin[2][kKC];
     __shared__ int s_w0[2][kKC];
     __shared__ float s_red[kThreads / 32][BB];
     __shared__ bool s_last;
+    __shared__ __align__(8) uint64_t full[2];  // ILM: bulk window copies of each buffer landed
+    constexpr int kAllJobs = (1 << NJ) - 1;
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
@@ -129,6 +133,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
                 for (int b = 0; b < BB; ++b) acc[j][p][q][b] = 0.f;
 
     const int nchunks = (a.m + kKC - 1) / kKC;
+    if constexpr (ILM != 0) {
+        if (threadIdx.x == 0) {
+            mbar_init(&full[0], 1);
+            mbar_init(&full[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
     // per-angle table + window staging of chunk ch into buffer bf
     auto stage = [&](int ch, int bf) {
         const int k0 = ch * kKC;
@@ -148,6 +160,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             }
         }
         __syncthreads();  // window origins visible
+        if constexpr (ILM != 0) {
+            // one bulk copy per (angle, job): kW bins x BB images, 16 B per bin, from the
+            // interleaved padded sinogram (in bounds for any window origin >= -kAdjPad; the
+            // pads supply the zeros outside [0, n_det))
+            if (threadIdx.x == 0) {
+                constexpr unsigned bytes = kW * BB * sizeof(float);
+                constexpr int nbulk = (ILM & 1) + ((ILM >> 1) & 1);
+                fence_proxy_async();  // generic reads of this buffer -> async-proxy writes
+                mbar_expect_tx(&full[bf], bytes * kc * nbulk);
+                const long wp = a.g.n_det + 2 * kAdjPad;
+                for (int t = 0; t < kc; ++t) {
+                    const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[bf][t];
+#pragma unroll
+                    for (int jj = 0; jj < NJ; ++jj)
+                        if ((ILM >> jj) & 1)
+                            bulk_g2s(&win[bf][jj][t * kW * BB], a.job[jj].pi + row * BB, bytes,
+                                     &full[bf]);
+                }
+            }
+        }
+        if constexpr (ILM == kAllJobs) return;
         // element e -> (angle t, bin w, image b), image fastest; zero outside [0, n_det)
         for (int e = threadIdx.x; e < kc * kW * BB; e += kThreads) {
             const int b = e % BB;
@@ -156,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             const int jb = s_w0[bf][t] + w;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
+                if ((ILM >> jj) & 1) continue;
                 float *dst = &win[bf][jj][e];
                 if (jb >= 0 && jb < n_det)
                     cp_async4(dst, a.job[jj].p + ((long)(b0 + b) * a.m + k0 + t) * n_det + jb);
@@ -169,11 +203,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
     stage(0, 0);
     for (int ch = 0; ch < nchunks; ++ch) {
         const int bf = ch & 1;
-        if (ch + 1 < nchunks) {
-            stage(ch + 1, bf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+        if (ch + 1 < nchunks) stage(ch + 1, bf ^ 1);
+        if constexpr (ILM != 0) mbar_wait(&full[bf], (unsigned)((ch >> 1) & 1));
+        if constexpr (ILM != kAllJobs) {
+            if (ch + 1 < nchunks)
+                cp_async_wait<1>();
+            else
+                cp_async_wait<0>();
         }
         __syncthreads();
         const int kc = min(kKC, a.m - ch * kKC);
@@ -283,10 +319,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
 template <int BB>
 cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
     dim3 grid((unsigned)(a.tiles_x * a.tiles_x), (unsigned)(B / BB), 1);
-    if (njobs == 2)
-        k_radon_adj<BB, 2><<<grid, kThreads, 0, s>>>(a);
-    else
-        k_radon_adj<BB, 1><<<grid, kThreads, 0, s>>>(a);
+    // bulk-copy staging needs 16-byte bins (BB = 4) and an interleaved source
+    const int ilm = BB != 4 ? 0 : (a.job[0].pi ? 1 : 0) | (njobs > 1 && a.job[1].pi ? 2 : 0);
+    constexpr int kB4 = BB == 4 ? 1 : 0;  // (the bulk variants are only instantiated for BB = 4)
+    if (njobs == 2) {
+        switch (ilm) {
+            case 3: k_radon_adj<BB, 2, 3 * kB4><<<grid, kThreads, 0, s>>>(a); break;
+            case 2: k_radon_adj<BB, 2, 2 * kB4><<<grid, kThreads, 0, s>>>(a); break;
+            case 1: k_radon_adj<BB, 2, 1 * kB4><<<grid, kThreads, 0, s>>>(a); break;
+            default: k_radon_adj<BB, 2, 0><<<grid, kThreads, 0, s>>>(a); break;
+        }
+    } else {
+        if (ilm)
+            k_radon_adj<BB, 1, kB4><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_radon_adj<BB, 1, 0><<<grid, kThreads, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

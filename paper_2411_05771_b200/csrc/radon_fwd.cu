@@ -47,6 +47,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "tma.h"
 
 namespace skei {
 namespace {
@@ -83,48 +84,9 @@ struct FwdArgs {
     unsigned *mc_ctr;
     float *mc_out;
     unsigned *queue;  // piece counters of the stream-K split units, indexed by the unit's
-                      // first cluster (< gridDim.x; zero before the launch, self-resetting)
-    float *scratch;   // per-CTA partial projections [gridDim.x][K * n_det * BB], then the
-                      // split-unit pieces [clusters][2][K * n_det * BB]
+                      // first CTA (< gridDim.x; zero before the launch, self-resetting)
+    float *scratch;   // split-unit pieces [gridDim.x][2][K * n_det * BB]
 };
-
-// ---- TMA bulk copy + mbarrier (sm_90+ async proxy), inline PTX
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-            "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until the phase
-    // completes (or the hint expires) instead of spinning on issue slots other warps need
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
 
 // One packed block (n pixel columns of 128 B) -> the interior of a staging buffer.
 __device__ __forceinline__ void issue_block(float *buf, const float *src, int n, uint64_t *bar) {

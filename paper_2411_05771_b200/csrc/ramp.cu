@@ -88,7 +88,21 @@ struct RampArgs {
     const float *R;    // [P] spectrum / P
     const float2 *tw;  // per-pass twiddle tables [k][r], k < Ns, r < R
     int npass;
+    // optional interleaved copy for the backprojector's bulk window copies:
+    // row (b, k) of q -> qi[b / BB][k][kAdjPad + j][b % BB], zero pads of kAdjPad bins on
+    // both sides (rows of width wp = n_det + 2 kAdjPad)
+    float *qi;
+    int m, bb, wp;
+    // optional: CTAs nramp.. copy the residual r [B][m][n_det] into the same interleaved
+    // layout (one CTA per (image group of 4, angle): 16-byte stores)
+    const float *rs;
+    float *ri;
+    int nramp;
 };
+__device__ __forceinline__ float *il_row(const RampArgs &a, int row) {
+    const int b = row / a.m, k = row - b * a.m;
+    return a.qi + ((long)((b / a.bb) * a.m + k) * a.wp + kAdjPad) * a.bb + b % a.bb;
+}
 
 // One Stockham pass (in place on z): J = 16/R butterflies per thread.  mode flags:
 // kIn = read the two input rows from global (first forward pass), kScale = multiply by
@@ -97,7 +111,7 @@ struct RampArgs {
 constexpr int kIn = 1, kScale = 2, kOut = 4;
 template <int R>
 __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool inverse, int mode,
-                                     const float *pa, const float *pb, float *qa, float *qb) {
+                                     const float *pa, const float *pb, float *qa, float *qb, float *ia, float *ib) {
     constexpr int J = 16 / R;
     // every pass before `ip` is radix 16: Ns = 16^ip, table offset = sum_{i<ip} 16 * 16^i
     const int Ns = 1 << (4 * ip), stride = a.P / R;
@@ -142,6 +156,10 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
                 if (o < a.n_det) {
                     qa[o] = v[jj][q].x;
                     if (qb) qb[o] = v[jj][q].y;
+                    if (ia) {
+                        ia[(long)o * a.bb] = v[jj][q].x;
+                        if (ib) ib[(long)o * a.bb] = v[jj][q].y;
+                    }
                 }
             }
         } else {
@@ -155,20 +173,45 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
 template <int RL>
 __global__ void __launch_bounds__(512) k_ramp(RampArgs a) {  // P/16 <= 512 threads
     extern __shared__ float2 z[];
+    if ((int)blockIdx.x >= a.nramp) {  // interleave r: group g = u / m of 4 images, angle k
+        const int u = blockIdx.x - a.nramp, g = u / a.m, k = u - g * a.m;
+        const long stride = (long)a.m * a.n_det;  // between images
+        const float *src = a.rs + ((long)(4 * g) * a.m + k) * a.n_det;
+        float4 *dst = reinterpret_cast<float4 *>(a.ri) + (long)u * a.wp;
+        for (int o = threadIdx.x; o < a.wp; o += blockDim.x) {
+            const int j = o - kAdjPad;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j >= 0 && j < a.n_det)
+                v = make_float4(__ldg(src + j), __ldg(src + stride + j), __ldg(src + 2 * stride + j),
+                                __ldg(src + 3 * stride + j));
+            dst[o] = v;
+        }
+        return;
+    }
     const int ra = 2 * blockIdx.x, rb = ra + 1;
     const bool has_b = rb < a.rows;
     const float *pa = a.p + (long)ra * a.n_det;
     const float *pb = has_b ? a.p + (long)rb * a.n_det : nullptr;
     float *qa = a.q + (long)ra * a.n_det;
     float *qb = has_b ? a.q + (long)rb * a.n_det : nullptr;
+    float *ia = a.qi ? il_row(a, ra) : nullptr;
+    float *ib = a.qi && has_b ? il_row(a, rb) : nullptr;
     const int last = a.npass - 1;
     // forward: radix-16 passes then the RL pass
-    for (int ip = 0; ip < last; ++ip) pass<16>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb);
-    pass<RL>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb);
+    for (int ip = 0; ip < last; ++ip)
+        pass<16>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib);
+    pass<RL>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib);
     // inverse of R . FFT(z)
     for (int ip = 0; ip < last; ++ip)
-        pass<16>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb);
-    pass<RL>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb);
+        pass<16>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb, ia, ib);
+    pass<RL>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb, ia, ib);
+    if (ia) {  // the zero pads of the interleaved rows
+        for (int t = threadIdx.x; t < 2 * kAdjPad; t += blockDim.x) {
+            const int o = t < kAdjPad ? t - kAdjPad : a.n_det + (t - kAdjPad);
+            ia[(long)o * a.bb] = 0.f;
+            if (ib) ib[(long)o * a.bb] = 0.f;
+        }
+    }
 }
 
 }  // namespace
@@ -199,8 +242,14 @@ void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal) 
 }
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
-                        cudaStream_t s) {
+                        cudaStream_t s, float *qi, int m, int bb, const float *rs, float *ri) {
     RampArgs a;
+    a.rs = rs;
+    a.ri = ri;
+    a.qi = qi;
+    a.m = m > 0 ? m : 1;
+    a.bb = bb > 0 ? bb : 1;
+    a.wp = plan->n_det + 2 * kAdjPad;
     a.p = p;
     a.q = q;
     a.rows = rows;
@@ -212,7 +261,9 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     const int RL = plan->fft_radix[plan->fft_npass - 1];
     const size_t smem = sizeof(float2) * (size_t)(a.P + a.P / 16);
     const int threads = a.P / 16;
-    const int grid = (rows + 1) / 2;
+    a.nramp = (rows + 1) / 2;
+    // + the interleaving CTAs of r (rows / m images in groups of 4, m angles each)
+    const int grid = a.nramp + (ri && rs ? (rows / a.m / 4) * a.m : 0);
     cudaError_t e = cudaSuccess;
 #define SKEI_RAMP_LAUNCH(RLV)                                                                   \
     do {                                                                                        \

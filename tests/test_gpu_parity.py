@@ -223,6 +223,21 @@ def test_pass_deterministic_bitwise():
         assert torch.equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_pass_backprojections_match_standalone_calls(name):
+    """With image groups of 4 the pass stages the backprojector's detector windows by bulk
+    copies from interleaved padded copies of q and r (written by the ramp launch); the
+    standalone calls stage them from the plain sinograms.  Same arithmetic: bit-identical."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = synth.make_workload(cfg)
+    g, idx = sk.draw_device(0, 3, 0, 1, True, cfg.n_full, cfg.m)
+    out = sk.sketched_pass(plan, dev(x1), dev(y), g, idx)
+    assert torch.equal(sk.ramp_filter(plan, out["p2"]), out["q"])
+    assert torch.equal(sk.fbp(plan, out["p2"], idx), out["xfbp"])
+    assert torch.equal(sk.radon_adj(plan, out["r"], idx, 2.0), out["grad"])
+
+
 def test_gpu_adjoint_identity():
     cfg = synth.CONFIGS["cfg2"]
     plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
