@@ -170,8 +170,9 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
     if (!(mode & kOut)) __syncthreads();
 }
 
-template <int RL>
-__global__ void __launch_bounds__(512) k_ramp(RampArgs a) {  // P/16 <= 512 threads
+// MAXT: P/16 <= MAXT threads; MINB: resident CTAs per SM the register budget must allow
+template <int RL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
     extern __shared__ float2 z[];
     if ((int)blockIdx.x >= a.nramp) {  // interleave r: group g = u / m of 4 images, angle k
         const int u = blockIdx.x - a.nramp, g = u / a.m, k = u - g * a.m;
@@ -265,12 +266,20 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     // + the interleaving CTAs of r (rows / m images in groups of 4, m angles each)
     const int grid = a.nramp + (ri && rs ? (rows / a.m / 4) * a.m : 0);
     cudaError_t e = cudaSuccess;
-#define SKEI_RAMP_LAUNCH(RLV)                                                                   \
+#define SKEI_RAMP_LAUNCH3(RLV, MT, MB)                                                          \
     do {                                                                                        \
         if (smem > 48 * 1024)                                                                   \
-            e = cudaFuncSetAttribute(k_ramp<RLV>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                     (int)smem);                                                \
-        if (e == cudaSuccess) k_ramp<RLV><<<grid, threads, smem, s>>>(a);                      \
+            e = cudaFuncSetAttribute(k_ramp<RLV, MT, MB>,                                       \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        if (e == cudaSuccess) k_ramp<RLV, MT, MB><<<grid, threads, smem, s>>>(a);              \
+    } while (0)
+    // small transforms (P <= 2048, <= 128 threads): <= 64 registers so 8 CTAs fit an SM
+#define SKEI_RAMP_LAUNCH(RLV)                      \
+    do {                                           \
+        if (threads <= 128)                        \
+            SKEI_RAMP_LAUNCH3(RLV, 128, 6);        \
+        else                                       \
+            SKEI_RAMP_LAUNCH3(RLV, 512, 1);        \
     } while (0)
     switch (RL) {
         case 16: SKEI_RAMP_LAUNCH(16); break;
@@ -279,6 +288,7 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
         default: SKEI_RAMP_LAUNCH(2); break;
     }
 #undef SKEI_RAMP_LAUNCH
+#undef SKEI_RAMP_LAUNCH3
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
