@@ -98,16 +98,15 @@ __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
     w2 = fmaxf(0.f, u - 1.f);
 }
 
-// ILM: bit jj set = job jj's windows are bulk copies from its interleaved padded sinogram
-template <int BB, int NJ, int ILM>
+// BULK: every job's windows are bulk copies from its interleaved padded sinogram (BB = 4)
+template <int BB, int NJ, bool BULK>
 __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
     __shared__ __align__(128) float win[2][NJ][kKC * kW * BB];
     __shared__ float s_off[2][kKC], s_cos[2][kKC], s_sin[2][kKC];
     __shared__ int s_w0[2][kKC];
     __shared__ float s_red[kThreads / 32][BB];
     __shared__ bool s_last;
-    __shared__ __align__(8) uint64_t full[2];  // ILM: bulk window copies of each buffer landed
-    constexpr int kAllJobs = (1 << NJ) - 1;
+    __shared__ __align__(8) uint64_t full[2];  // BULK: window copies of each buffer landed
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
                 for (int b = 0; b < BB; ++b) acc[j][p][q][b] = 0.f;
 
     const int nchunks = (a.m + kKC - 1) / kKC;
-    if constexpr (ILM != 0) {
+    if constexpr (BULK) {
         if (threadIdx.x == 0) {
             mbar_init(&full[0], 1);
             mbar_init(&full[1], 1);
@@ -141,47 +140,46 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
         }
         __syncthreads();
     }
-    // per-angle table + window staging of chunk ch into buffer bf
+    // per-angle table of chunk ch (threads < kKC): window origin, fp64 -> split precision
+    auto table = [&](int ch, int bf) {
+        const int k0 = ch * kKC;
+        const int kc = min(kKC, a.m - k0);
+        if (threadIdx.x < kc) {
+            const double2 cs = a.g.trig[idx[k0 + threadIdx.x]];
+            // detector position of the tile origin pixel (tr0, tc0), fp64
+            const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
+            const double jmin = J0 + fmin(0.0, (kTile - 1) * cs.x) + fmin(0.0, -(kTile - 1) * cs.y);
+            const double w0 = floor(jmin);
+            s_off[bf][threadIdx.x] = (float)(J0 - w0);
+            s_cos[bf][threadIdx.x] = (float)cs.x;
+            s_sin[bf][threadIdx.x] = (float)cs.y;
+            s_w0[bf][threadIdx.x] = (int)w0;
+        }
+    };
+    // bulk path (thread 0): one bulk copy per (angle, job): kW bins x BB images, 16 B per bin,
+    // from the interleaved padded sinogram (in bounds for any window origin >= -kAdjPad; the
+    // pads supply the zeros outside [0, n_det)); completion on full[bf]
+    auto issue_bulk = [&](int ch, int bf) {
+        const int k0 = ch * kKC;
+        const int kc = min(kKC, a.m - k0);
+        constexpr unsigned bytes = kW * BB * sizeof(float);
+        fence_proxy_async();  // earlier generic reads of this buffer -> async-proxy writes
+        mbar_expect_tx(&full[bf], bytes * kc * NJ);
+        const long wp = a.g.n_det + 2 * kAdjPad;
+        for (int t = 0; t < kc; ++t) {
+            const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[bf][t];
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj)
+                bulk_g2s(&win[bf][jj][t * kW * BB], a.job[jj].pi + row * BB, bytes, &full[bf]);
+        }
+    };
+    // plain path (all threads): table, then element-wise cp.async, zero outside [0, n_det)
     auto stage = [&](int ch, int bf) {
         const int k0 = ch * kKC;
         const int kc = min(kKC, a.m - k0);
-        if (threadIdx.x < kKC) {
-            if (threadIdx.x < kc) {
-                const double2 cs = a.g.trig[idx[k0 + threadIdx.x]];
-                // detector position of the tile origin pixel (tr0, tc0), fp64
-                const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
-                const double jmin =
-                    J0 + fmin(0.0, (kTile - 1) * cs.x) + fmin(0.0, -(kTile - 1) * cs.y);
-                const double w0 = floor(jmin);
-                s_off[bf][threadIdx.x] = (float)(J0 - w0);
-                s_cos[bf][threadIdx.x] = (float)cs.x;
-                s_sin[bf][threadIdx.x] = (float)cs.y;
-                s_w0[bf][threadIdx.x] = (int)w0;
-            }
-        }
+        table(ch, bf);
         __syncthreads();  // window origins visible
-        if constexpr (ILM != 0) {
-            // one bulk copy per (angle, job): kW bins x BB images, 16 B per bin, from the
-            // interleaved padded sinogram (in bounds for any window origin >= -kAdjPad; the
-            // pads supply the zeros outside [0, n_det))
-            if (threadIdx.x == 0) {
-                constexpr unsigned bytes = kW * BB * sizeof(float);
-                constexpr int nbulk = (ILM & 1) + ((ILM >> 1) & 1);
-                fence_proxy_async();  // generic reads of this buffer -> async-proxy writes
-                mbar_expect_tx(&full[bf], bytes * kc * nbulk);
-                const long wp = a.g.n_det + 2 * kAdjPad;
-                for (int t = 0; t < kc; ++t) {
-                    const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[bf][t];
-#pragma unroll
-                    for (int jj = 0; jj < NJ; ++jj)
-                        if ((ILM >> jj) & 1)
-                            bulk_g2s(&win[bf][jj][t * kW * BB], a.job[jj].pi + row * BB, bytes,
-                                     &full[bf]);
-                }
-            }
-        }
-        if constexpr (ILM == kAllJobs) return;
-        // element e -> (angle t, bin w, image b), image fastest; zero outside [0, n_det)
+        // element e -> (angle t, bin w, image b), image fastest
         for (int e = threadIdx.x; e < kc * kW * BB; e += kThreads) {
             const int b = e % BB;
             const int w = (e / BB) % kW;
@@ -189,7 +187,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             const int jb = s_w0[bf][t] + w;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
-                if ((ILM >> jj) & 1) continue;
                 float *dst = &win[bf][jj][e];
                 if (jb >= 0 && jb < n_det)
                     cp_async4(dst, a.job[jj].p + ((long)(b0 + b) * a.m + k0 + t) * n_det + jb);
@@ -199,19 +196,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
         }
         cp_async_commit();
     };
+    // warp 0 prepares chunk ch in buffer bf: its lanes write the table, lane 0 (after the
+    // warp barrier) issues the copies; the other warps see the table through the mbarrier
+    // (arrive.release by lane 0, try_wait.acquire by the consumers)
+    auto produce = [&](int ch, int bf) {
+        if (warp == 0) {
+            table(ch, bf);
+            __syncwarp();
+            if (lane == 0) issue_bulk(ch, bf);
+        }
+    };
 
-    stage(0, 0);
+    if constexpr (BULK) {
+        produce(0, 0);
+        if (nchunks > 1) produce(1, 1);
+    } else {
+        stage(0, 0);
+    }
     for (int ch = 0; ch < nchunks; ++ch) {
         const int bf = ch & 1;
-        if (ch + 1 < nchunks) stage(ch + 1, bf ^ 1);
-        if constexpr (ILM != 0) mbar_wait(&full[bf], (unsigned)((ch >> 1) & 1));
-        if constexpr (ILM != kAllJobs) {
+        if constexpr (BULK) {
+            mbar_wait(&full[bf], (unsigned)((ch >> 1) & 1));
+        } else {
+            if (ch + 1 < nchunks) stage(ch + 1, bf ^ 1);
             if (ch + 1 < nchunks)
                 cp_async_wait<1>();
             else
                 cp_async_wait<0>();
+            __syncthreads();
         }
-        __syncthreads();
         const int kc = min(kKC, a.m - ch * kKC);
 #pragma unroll 2
         for (int t = 0; t < kc; ++t) {
@@ -242,7 +255,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
                 }
             }
         }
-        __syncthreads();  // buffer bf is free for chunk ch + 2
+        __syncthreads();  // buffer bf (and its table) is free for chunk ch + 2
+        if constexpr (BULK) {
+            if (ch + 2 < nchunks) produce(ch + 2, bf);
+        }
     }
 
     // ---- epilogue: scale and store; optional fused ei partials (job 0 = FBP)
@@ -319,21 +335,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
 template <int BB>
 cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
     dim3 grid((unsigned)(a.tiles_x * a.tiles_x), (unsigned)(B / BB), 1);
-    // bulk-copy staging needs 16-byte bins (BB = 4) and an interleaved source
-    const int ilm = BB != 4 ? 0 : (a.job[0].pi ? 1 : 0) | (njobs > 1 && a.job[1].pi ? 2 : 0);
-    constexpr int kB4 = BB == 4 ? 1 : 0;  // (the bulk variants are only instantiated for BB = 4)
+    // bulk-copy staging needs 16-byte bins (BB = 4) and interleaved sources for every job
+    constexpr bool kB4 = BB == 4;  // (the bulk variants are only instantiated for BB = 4)
+    const bool bulk = kB4 && a.job[0].pi && (njobs == 1 || a.job[1].pi);
     if (njobs == 2) {
-        switch (ilm) {
-            case 3: k_radon_adj<BB, 2, 3 * kB4><<<grid, kThreads, 0, s>>>(a); break;
-            case 2: k_radon_adj<BB, 2, 2 * kB4><<<grid, kThreads, 0, s>>>(a); break;
-            case 1: k_radon_adj<BB, 2, 1 * kB4><<<grid, kThreads, 0, s>>>(a); break;
-            default: k_radon_adj<BB, 2, 0><<<grid, kThreads, 0, s>>>(a); break;
-        }
+        if (bulk)
+            k_radon_adj<BB, 2, kB4><<<grid, kThreads, 0, s>>>(a);
+        else
+            k_radon_adj<BB, 2, false><<<grid, kThreads, 0, s>>>(a);
     } else {
-        if (ilm)
+        if (bulk)
             k_radon_adj<BB, 1, kB4><<<grid, kThreads, 0, s>>>(a);
         else
-            k_radon_adj<BB, 1, 0><<<grid, kThreads, 0, s>>>(a);
+            k_radon_adj<BB, 1, false><<<grid, kThreads, 0, s>>>(a);
     }
     return cudaGetLastError();
 }
