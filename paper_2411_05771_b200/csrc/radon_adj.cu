@@ -3,22 +3,24 @@
 // gather over angles with the sketched angle table in shared memory").
 //
 // Design (DESIGN.md §7 "k_radon_adj"):
-//   * One CTA = a 32 x 32 pixel tile x BB images sharing one angle list x all jobs of the
+//   * One CTA = a 32 x 16 pixel tile x BB images sharing one angle list x all jobs of the
 //     launch (the pass runs the FBP of q and the MC gradient of r as two jobs: they share
-//     the geometry, so it is computed once for 2*BB images).
-//   * Each thread owns two pairs of horizontally adjacent pixels (c, c+1) of one row.  The
+//     the geometry, so it is computed once for 2*BB images); 256 threads, 4 CTAs per SM.
+//   * Each thread owns one pair of horizontally adjacent pixels (c, c+1) of one row.  The
 //     detector positions t and t + cos(th) of a pair lie within one 3-bin window [j, j+3),
 //     so a pair reads 3 bins per job (not 4) and interpolates each pixel with the 3 hat
 //     weights max(0, 1 - |t - j - k|) (one of which is 0).
 //   * Angles are processed in chunks of KC.  For each angle the CTA stages the W-bin detector
 //     window of the tile, interleaved [bin][image] (one LDS.128 = a bin of 4 images), zero
-//     outside [0, n_det) so dropped taps need no branch; chunks are double-buffered with
-//     cp.async so the next chunk's loads overlap this chunk's gathers.
+//     outside [0, n_det) so dropped taps need no branch; double-buffered.  In the fused pass
+//     (BULK) each window is one bulk copy from interleaved zero-padded copies of q and r that
+//     warp 0 issues two chunks ahead (one barrier per chunk); standalone calls stage them
+//     from the plain sinograms with cp.async.
 //   * Bank-conflict-free gathers: the 8 lanes of a shared-memory phase are 8 consecutive rows
 //     of one pixel column pair; their bins move by |sin th| <= 1 per row, so they span <= 8
 //     consecutive 16-byte slots (distinct banks, equal slots broadcast).
 //   * Positions in split precision: the fp64 tile-origin position per angle plus an fp32
-//     local offset < 48 px.
+//     local offset < 40 px.
 //   * Optional fused epilogue (skei_pass with the identity network): ei partial sums
 //     sum (x2 - x_fbp)^2 per tile and image, reduced in fixed order by the last CTA.
 // Work per (pixel, angle, image) = 2 taps; per pixel pair and angle 3 LDS.BB per job.
@@ -28,16 +30,17 @@
 namespace skei {
 namespace {
 
-constexpr int kTile = 32;      // tile side (pixels)
-constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 16 columns (8 pixel pairs)
-constexpr int kPairs = 2;      // pixel pairs per thread
+constexpr int kTileW = 32;     // tile width (columns)
+constexpr int kTileH = 16;     // tile height (rows)
+constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 8 columns (4 pixel pairs)
+constexpr int kPairs = 1;      // pixel pairs per thread
 constexpr int kKC = 12;        // angles per staged chunk (2 buffers x 2 jobs fit 48 KB)
-constexpr int kW = 48;         // staged bins per angle (>= 31 sqrt 2 + 3)
+constexpr int kW = 40;         // staged bins per angle (>= sqrt(31^2 + 15^2) + 3)
 
 struct AdjArgs {
     AdjJob job[2];
     const int32_t *idx;
-    int m, idx_stride, B, tiles_x;
+    int m, idx_stride, B, tiles_x, tiles_y;
     Geom g;
     // fused ei epilogue (job 0 = FBP): x2 [B][n][n], partials [B][ntiles], counter, ei [B]
     const float *ei_x2;
@@ -100,7 +103,7 @@ __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
 
 // BULK: every job's windows are bulk copies from its interleaved padded sinogram (BB = 4)
 template <int BB, int NJ, bool BULK>
-__global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     __shared__ __align__(128) float win[2][NJ][kKC * kW * BB];
     __shared__ float s_off[2][kKC], s_cos[2][kKC], s_sin[2][kKC];
     __shared__ int s_w0[2][kKC];
@@ -110,15 +113,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
-    const int tr0 = (tile / a.tiles_x) * kTile, tc0 = (tile % a.tiles_x) * kTile;
+    const int tr0 = (tile / a.tiles_x) * kTileH, tc0 = (tile % a.tiles_x) * kTileW;
     const int b0 = blockIdx.y * BB;
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp w: rows 8*(w/2) .. +7, pixel pairs 8*(w%2) .. +7; lane: row (lane % 8), pairs
     // (lane / 8) and (lane / 8) + 4 — the 8 lanes of a quarter-warp are 8 consecutive rows
     // of one pair
-    const int ry = 8 * (warp >> 1) + (lane & 7);
-    const int pc0 = 8 * (warp & 1) + (lane >> 3);  // pair index 0..15, second pair = +4
+    const int ry = 8 * (warp & 1) + (lane & 7);
+    const int pc0 = 4 * (warp >> 1) + (lane >> 3);  // pair index 0..15
     const long nn = (long)n * n;
 
     float acc[NJ][kPairs][2][BB];  // [job][pair][pixel][image]
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             const double2 cs = a.g.trig[idx[k0 + threadIdx.x]];
             // detector position of the tile origin pixel (tr0, tc0), fp64
             const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
-            const double jmin = J0 + fmin(0.0, (kTile - 1) * cs.x) + fmin(0.0, -(kTile - 1) * cs.y);
+            const double jmin = J0 + fmin(0.0, (kTileW - 1) * cs.x) + fmin(0.0, -(kTileH - 1) * cs.y);
             const double w0 = floor(jmin);
             s_off[bf][threadIdx.x] = (float)(J0 - w0);
             s_cos[bf][threadIdx.x] = (float)cs.x;
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
             const float rowb = fmaf(-(float)ry, st, s_off[bf][t]);
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) {
-                const int c = 2 * (pc0 + 4 * p);
+                const int c = 2 * (pc0 + 16 * p);
                 const float t1 = fmaf((float)c, ct, rowb);
                 const float t2 = t1 + ct;
                 const float lo = fmaxf(fminf(t1, t2), 0.f);
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
         const float sc = a.job[jj].scale;
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) {
-            const int c = tc0 + 2 * (pc0 + 4 * p);
+            const int c = tc0 + 2 * (pc0 + 16 * p);
             if (r >= n) continue;
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_radon_adj(AdjArgs a) {
 
 template <int BB>
 cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
-    dim3 grid((unsigned)(a.tiles_x * a.tiles_x), (unsigned)(B / BB), 1);
+    dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)(B / BB), 1);
     // bulk-copy staging needs 16-byte bins (BB = 4) and interleaved sources for every job
     constexpr bool kB4 = BB == 4;  // (the bulk variants are only instantiated for BB = 4)
     const bool bulk = kB4 && a.job[0].pi && (njobs == 1 || a.job[1].pi);
@@ -355,8 +358,8 @@ cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
 }  // namespace
 
 size_t adj_ei_part_floats(const skei_plan *plan, int B) {
-    const int t = (plan->n + kTile - 1) / kTile;
-    return (size_t)B * t * t;
+    const int tx = (plan->n + kTileW - 1) / kTileW, ty = (plan->n + kTileH - 1) / kTileH;
+    return (size_t)B * tx * ty;
 }
 
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
@@ -370,7 +373,8 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
     a.idx_stride = idx_stride;
     a.B = B;
     a.g = geom_of(plan);
-    a.tiles_x = (plan->n + kTile - 1) / kTile;
+    a.tiles_x = (plan->n + kTileW - 1) / kTileW;
+    a.tiles_y = (plan->n + kTileH - 1) / kTileH;
     a.ei_x2 = ei ? ei->x2 : nullptr;
     a.ei_part = ei ? ei->part : nullptr;
     a.ei_ctr = ei ? ei->ctr : nullptr;
