@@ -469,12 +469,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #ifdef SKEI_FWD_STATS
             st_wait += clock64() - tw0;
 #endif
+            int4 tdn = s_task[warp];  // the next task's descriptor, loaded one task ahead
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
-                const int4 td = s_task[warp + kWarps * t];  // warp-uniform (broadcast)
+                const int4 td = tdn;  // warp-uniform (broadcast)
                 const int k = td.x;
                 if (k < 0) break;
                 const int4 ent = btab[k * nbu + i];
+                if (t + 1 < kMaxT) tdn = s_task[warp + kWarps * (t + 1)];
                 if (td.y > ent.w || td.y + 31 < ent.z) continue;  // chunk misses the block
 #ifdef SKEI_FWD_STATS
                 ++st_active;
