@@ -50,6 +50,8 @@ def _load():
         lib.oracle_draw.restype = i32
         lib.oracle_draw.argtypes = [u64, u64, u64, i32, i32, i32, ip, ip]
         lib.oracle_rotate.argtypes = [dp, dp, i32, i32]
+        lib.oracle_rotate_adj.argtypes = [dp, dp, i32, i32]
+        lib.oracle_ei_grad.argtypes = [dp, i32, i32, i32, i32, ip, i32, dp]
         lib.oracle_fwd.argtypes = [dp, dp, i32, i32, i32, ip, i32]
         lib.oracle_adj.argtypes = [dp, dp, i32, i32, i32, ip, i32, ctypes.c_double]
         lib.oracle_ramp.argtypes = [dp, dp, i32, i32]
@@ -102,6 +104,26 @@ def rotate(x, g: int):
     flat_in, flat_out = x.reshape(-1, N, N), out.reshape(-1, N, N)
     for b in range(flat_in.shape[0]):
         _load().oracle_rotate(_dp(flat_in[b]), _dp(flat_out[b]), N, int(g))
+    return out
+
+
+def rotate_adj(y, g: int):
+    """T_g^T y (oracle.c oracle_rotate_adj) for one image or a batch sharing g."""
+    y = _d(y)
+    out = np.empty_like(y)
+    N = y.shape[-1]
+    flat_in, flat_out = y.reshape(-1, N, N), out.reshape(-1, N, N)
+    for b in range(flat_in.shape[0]):
+        _load().oracle_rotate_adj(_dp(flat_in[b]), _dp(flat_out[b]), N, int(g))
+    return out
+
+
+def ei_grad(x1, g: int, idx, n_full: int, n_det: int):
+    """d ||x2 - x3||^2 / d x1 for one image, identity network (oracle.c oracle_ei_grad)."""
+    x1, idx = _d(x1), _i(idx)
+    N = x1.shape[-1]
+    out = np.empty((N, N))
+    _load().oracle_ei_grad(_dp(x1), N, n_det, n_full, int(g), _ip(idx), len(idx), _dp(out))
     return out
 
 

@@ -140,6 +140,39 @@ void oracle_rotate(const double *x, double *out, int N, int g)
     }
 }
 
+/* ------------------------------------------ rotation transpose (R11, §8(f) #1) --
+ * out = T_g^T y: the transpose of oracle_rotate, written as a SCATTER: every output
+ * pixel (r, c) of the rotation hands y[r][c] back to the (in-grid) bilinear neighbours
+ * of its source position with the same weights.  It is what the EI term's gradient
+ * needs to pass d||x2 - x3||^2 / dx2 back through x2 = T_g x1 (Eq. 6,
+ * Alg. 1 steps 4-6 L120-L122). */
+void oracle_rotate_adj(const double *y, double *out, int N, int g)
+{
+    double cg, sg;
+    oracle_cossin_deg(g, &cg, &sg);
+    double h = (N - 1) / 2.0;
+    for (long i = 0; i < (long)N * N; ++i) out[i] = 0.0;
+    for (int r = 0; r < N; ++r) {
+        for (int c = 0; c < N; ++c) {
+            double u = c - h, v = h - r;
+            double us = u * cg + v * sg;
+            double vs = -u * sg + v * cg;
+            double cs = us + h, rs = h - vs;
+            double r0 = floor(rs), c0 = floor(cs);
+            double a = rs - r0, b = cs - c0;
+            double val = y[(long)r * N + c];
+            for (int dr = 0; dr < 2; ++dr) {
+                for (int dc = 0; dc < 2; ++dc) {
+                    long rr = (long)r0 + dr, cc = (long)c0 + dc;
+                    if (rr < 0 || rr >= N || cc < 0 || cc >= N) continue;
+                    double w = (dr ? a : 1.0 - a) * (dc ? b : 1.0 - b);
+                    out[rr * N + cc] += w * val;
+                }
+            }
+        }
+    }
+}
+
 /* ------------------------------------------------------- forward A_S (R1-R4) --
  * p[k][j] = sum_{r,c} x[r][c] * max(0, 1 - |u_c cos th + v_r sin th - s_j|),
  * th = idx[k] * pi / n_full, u_c = c-(N-1)/2, v_r = (N-1)/2-r, s_j = j-(n_det-1)/2
@@ -301,4 +334,35 @@ void oracle_pass(const double *x1, const double *y, int N, int n_det, int n_full
     if (!q) free(bq);
     if (!xfbp) free(bxf);
     if (!r) free(br);
+}
+
+/* --------------------------------------- EI-branch gradient (R16, §8(f) #1) --
+ * grad = d ||x2 - x3||^2 / d x1 for x2 = T_g x1 and the identity network
+ * x3 = M x2, M = (pi/2m) A_S^T H2 A_S (the sketched FBP of the sketched projection,
+ * Alg. 1 step 5 L121; R16).  ei = ||(I - M) T_g x1||^2 and M is symmetric (H2 is an
+ * even kernel, A_S^T is the transpose of A_S), so
+ *   grad = T_g^T (I - M) d,  d = 2 (x2 - x3),
+ * evaluated step by step with the routines above (Eq. 6). */
+void oracle_ei_grad(const double *x1, int N, int n_det, int n_full, int g, const int *idx,
+                    int m, double *grad)
+{
+    size_t nn = (size_t)N * N, mn = (size_t)m * n_det;
+    double *x2 = (double *)malloc(sizeof(double) * nn);
+    double *x3 = (double *)malloc(sizeof(double) * nn);
+    double *d = (double *)malloc(sizeof(double) * nn);
+    double *md = (double *)malloc(sizeof(double) * nn);
+    double *p = (double *)malloc(sizeof(double) * mn);
+    oracle_rotate(x1, x2, N, g);
+    oracle_fwd(x2, p, N, n_det, n_full, idx, m);
+    oracle_fbp(p, x3, N, n_det, n_full, idx, m, m);        /* x3 = M x2 */
+    for (size_t i = 0; i < nn; ++i) d[i] = 2.0 * (x2[i] - x3[i]);
+    oracle_fwd(d, p, N, n_det, n_full, idx, m);
+    oracle_fbp(p, md, N, n_det, n_full, idx, m, m);        /* M d */
+    for (size_t i = 0; i < nn; ++i) d[i] -= md[i];        /* (I - M) d */
+    oracle_rotate_adj(d, grad, N, g);
+    free(x2);
+    free(x3);
+    free(d);
+    free(md);
+    free(p);
 }

@@ -409,3 +409,88 @@ def test_whole_pass_dense_8x8():
         assert np.max(np.abs(out[name].ravel() - ref)) < 1e-12, name
     assert abs(out["mc"] - rr @ rr) < 1e-12 * (rr @ rr)
     assert abs(out["ei"] - np.sum((x2 - xf) ** 2)) < 1e-12 * np.sum((x2 - xf) ** 2)
+
+
+# ------------------------------------------------- EI-branch backward
+def _dense_T(N, g):
+    """Dense bilinear rotation from scipy (map_coordinates, order 1, zeros outside) applied
+    to the basis images — independent of oracle_rotate."""
+    h = (N - 1) / 2
+    r, c = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    u, v = c - h, h - r
+    cg, sg = math.cos(math.radians(g)), math.sin(math.radians(g))
+    coords = [h - (-u * sg + v * cg), u * cg + v * sg + h]
+    return np.stack([ndi.map_coordinates(np.eye(N * N)[i].reshape(N, N), coords, order=1,
+                                         mode="grid-constant").ravel() for i in range(N * N)], 1)
+
+
+@pytest.mark.parametrize("g", [37, 123, 211, 300])
+def test_rotation_transpose_dense_8x8(g):
+    """T_g^T: oracle_rotate_adj applied to every basis image equals the transpose of the
+    dense scipy rotation matrix (brute force)."""
+    N = 8
+    T = _dense_T(N, g)
+    TT = np.stack([oracle.rotate_adj(np.eye(N * N)[i].reshape(N, N), g).ravel()
+                   for i in range(N * N)], 1)
+    assert np.max(np.abs(TT - T.T)) < 1e-14
+
+
+@pytest.mark.parametrize("g", [1, 45, 89, 137, 359])
+def test_rotation_transpose_adjoint_identity(g):
+    """<T_g x, y> = <x, T_g^T y> for random x, y (33 x 33, odd size: the centre is a pixel)."""
+    rng = np.random.default_rng(g)
+    x, y = rng.standard_normal((33, 33)), rng.standard_normal((33, 33))
+    lhs = float(np.sum(oracle.rotate(x, g) * y))
+    rhs = float(np.sum(x * oracle.rotate_adj(y, g)))
+    assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(x) * np.linalg.norm(y)
+
+
+def test_rotation_transpose_quarter_turns_exact():
+    """The quarter turns are permutations, so their transposes are the inverse turns:
+    T_360^T = I, T_90^T = numpy rot90(., -1), T_180^T = rot90(., 2), T_270^T = rot90(., 1)."""
+    y = np.random.default_rng(3).standard_normal((16, 16))
+    assert np.array_equal(oracle.rotate_adj(y, 360), y)
+    assert np.array_equal(oracle.rotate_adj(y, 90), np.rot90(y, -1))
+    assert np.array_equal(oracle.rotate_adj(y, 180), np.rot90(y, 2))
+    assert np.array_equal(oracle.rotate_adj(y, 270), np.rot90(y, 1))
+
+
+def test_ei_gradient_dense_8x8():
+    """grad_x1 ||x2 - x3||^2 with x2 = T x1, x3 = M x2, M = (pi/2m) A^T H2 A, from dense
+    matrices: 2 T^T (I - M)^T (I - M) T x1 (scipy rotation, formula A, closed-form H2)."""
+    N, n_det, n_full, g = 8, 12, 8, 37
+    idx = np.array([1, 2, 5, 7])
+    m = len(idx)
+    T = _dense_T(N, g)
+    A = _dense_A(N, n_det, n_full, idx)
+    lag = np.arange(n_det)[:, None] - np.arange(n_det)[None, :]
+    H = np.where(lag == 0, 0.5, np.where(lag % 2 == 0, 0.0,
+                                         -2 / (np.pi ** 2 * np.maximum(np.abs(lag), 1) ** 2)))
+    M = (np.pi / (2 * m)) * A.T @ np.kron(np.eye(m), H) @ A
+    x1 = np.random.default_rng(9).standard_normal(N * N)
+    I = np.eye(N * N)
+    ref = 2 * T.T @ (I - M).T @ (I - M) @ T @ x1
+    got = oracle.ei_grad(x1.reshape(N, N), g, idx, n_full, n_det).ravel()
+    assert np.max(np.abs(got - ref)) < 1e-12 * max(1.0, np.max(np.abs(ref)))
+    assert np.max(np.abs(M - M.T)) < 1e-14  # the sketched FBP-of-projection is symmetric
+
+
+def test_ei_gradient_finite_difference():
+    """d/dx1 ei with ei from oracle_pass (identity network); ei is quadratic in x1, so
+    central differences are exact up to rounding."""
+    N, n_full, n_det, g = 12, 16, 17, 73
+    idx = np.array([0, 3, 5, 8, 13])
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((N, N))
+    y = rng.standard_normal((n_full, n_det))
+    grad = oracle.ei_grad(x, g, idx, n_full, n_det)
+
+    def ei(z):
+        return oracle.sketched_pass(z, y, g, idx, n_full)["ei"]
+
+    eps = 1e-3
+    for (r, c) in ((0, 0), (5, 7), (11, 3), (6, 6), (2, 9)):
+        e = np.zeros((N, N))
+        e[r, c] = eps
+        fd = (ei(x + e) - ei(x - e)) / (2 * eps)
+        assert abs(fd - grad[r, c]) <= 1e-8 * max(1.0, abs(fd))
