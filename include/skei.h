@@ -121,6 +121,41 @@ skei_status skei_draw_device(uint64_t seed, uint64_t iter, uint64_t image0, int3
 skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32_t B,
                         const int32_t *g_deg, int32_t g_stride, skei_stream stream);
 
+/* --------------------------------- next row: rotation transpose --
+ * out = T_g^T y, the exact transpose of skei_rotate (the bilinear weights handed back
+ * from every output pixel to the in-grid neighbours of its source position), needed to
+ * carry the EI term's gradient through x2 = T_g x1 (Eq. 6, Alg. 1
+ * steps 4-6 L120-L122).  Computed as a per-pixel gather over the <= 16 output pixels
+ * whose source can touch it (no atomics, deterministic).  Source positions in fp64.
+ * g_deg, g_stride, y, out as skei_rotate; out must not alias y.
+ * Errors: SKEI_ERR_ARG (NULL, g_stride, aliasing), SKEI_ERR_SHAPE (B < 1). */
+skei_status skei_rotate_adjoint(const skei_plan *plan, const float *y, float *out, int32_t B,
+                                const int32_t *g_deg, int32_t g_stride, skei_stream stream);
+
+/* ------------------------- next row: the EI branch's gradient --
+ * grad = d ||x2 - x3||^2 / d x1 for x2 = T_g x1 and the identity network
+ * x3 = M x2, M = (pi/2m) A_S^T ramp A_S (the sketched FBP, R16; Eq. 6
+ * L97-L101, Alg. 1 steps 4-6 L120-L122).  M is symmetric, so
+ *   grad = T_g^T (I - M) d,   d = 2 (x2 - x3),
+ * computed as: d (packed for the projector), A_S d, ramp, u = d - (pi/2m) A_S^T q,
+ * T_g^T u — five launches on `stream`.  x2, x3: [B][n][n] device (skei_pass's x2 and
+ * xfbp); g_deg, g_stride as skei_rotate; idx, m, idx_stride as skei_radon_fwd;
+ * grad: [B][n][n] device, must not alias x2 or x3; ws >= skei_workspace_bytes(plan, B, m).
+ * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL, strides,
+ * aliasing, ws too small). */
+/* The transpose of skei_fbp (next row): p = (pi / 2 m_total) ramp(A_S x)
+ * (the ramp kernel is even, so ramp is symmetric), i.e. the vector-Jacobian product of
+ * the sketched FBP.  x: [B][n][n], p: [B][m][n_det] device; other arguments and errors as
+ * skei_fbp. */
+skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, int32_t B,
+                             const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
+                             void *ws, size_t ws_bytes, skei_stream stream);
+
+skei_status skei_ei_grad(const skei_plan *plan, int32_t B, const float *x2, const float *x3,
+                         const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                         int32_t idx_stride, float *grad, void *ws, size_t ws_bytes,
+                         skei_stream stream);
+
 /* ------------------------------------------------------ a3: forward A_S --------
  * p[b][k][j] = sum_{r,c} x[b][r][c] * max(0, 1 - |u_c cos th + v_r sin th - s_j|),
  * th = theta_{idx_b[k]} (BASELINE.json north_star projector; PAPER.md L283

@@ -76,6 +76,9 @@ def lib():
             "skei_draw": ([u64, u64, u64, i32, i32, i32, vp, vp], st),
             "skei_draw_device": ([u64, u64, u64, i32, i32, i32, i32, i32, vp, vp, vp], st),
             "skei_rotate": ([vp, vp, vp, i32, vp, i32, vp], st),
+            "skei_rotate_adjoint": ([vp, vp, vp, i32, vp, i32, vp], st),
+            "skei_ei_grad": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, vp, sz, vp], st),
+            "skei_fbp_adjoint": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
             "skei_radon_adj": ([vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, vp], st),
             "skei_ramp_filter": ([vp, vp, vp, i32, vp], st),
@@ -211,6 +214,45 @@ def rotate(plan: Plan, x: torch.Tensor, g: torch.Tensor, out: torch.Tensor | Non
     g_stride = 0 if g.numel() == 1 else 1
     _check(lib().skei_rotate(plan.handle, _ptr(x, name="x"), _ptr(out, name="out"), B,
                              _ptr(g, torch.int32, "g"), g_stride, _stream(x)), "skei_rotate")
+    return out
+
+
+def rotate_adjoint(plan: Plan, y: torch.Tensor, g: torch.Tensor, out: torch.Tensor | None = None):
+    """skei_rotate_adjoint: T_g^T y (the transpose of `rotate`)."""
+    B = y.shape[0]
+    out = torch.empty_like(y) if out is None else out
+    g_stride = 0 if g.numel() == 1 else 1
+    _check(lib().skei_rotate_adjoint(plan.handle, _ptr(y, name="y"), _ptr(out, name="out"), B,
+                                     _ptr(g, torch.int32, "g"), g_stride, _stream(y)),
+           "skei_rotate_adjoint")
+    return out
+
+
+def fbp_adjoint(plan: Plan, x: torch.Tensor, idx: torch.Tensor, m_total: int | None = None,
+                out: torch.Tensor | None = None, ws: torch.Tensor | None = None):
+    """skei_fbp_adjoint: (pi / 2 m_total) ramp(A_S x), the transpose of `fbp`."""
+    B, m = x.shape[0], idx.shape[-1]
+    p = torch.empty(B, m, plan.n_det, dtype=torch.float32, device=x.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    _check(lib().skei_fbp_adjoint(plan.handle, _ptr(x, name="x"), _ptr(p, name="p"), B,
+                                  _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                  int(m_total or m), _ptr(ws, torch.uint8, "ws"), ws.numel(),
+                                  _stream(x)), "skei_fbp_adjoint")
+    return p
+
+
+def ei_grad(plan: Plan, x2: torch.Tensor, x3: torch.Tensor, g: torch.Tensor, idx: torch.Tensor,
+            out: torch.Tensor | None = None, ws: torch.Tensor | None = None):
+    """skei_ei_grad: d ||x2 - x3||^2 / d x1 for x2 = T_g x1 and the identity network
+    x3 = (pi/2m) A_S^T ramp A_S x2 (pass x2 and xfbp of the same draw)."""
+    B, m = x2.shape[0], idx.shape[-1]
+    out = torch.empty_like(x2) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    _check(lib().skei_ei_grad(plan.handle, B, _ptr(x2, name="x2"), _ptr(x3, name="x3"),
+                              _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,
+                              _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                              _ptr(out, name="grad"), _ptr(ws, torch.uint8, "ws"), ws.numel(),
+                              _stream(x2)), "skei_ei_grad")
     return out
 
 

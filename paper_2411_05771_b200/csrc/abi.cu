@@ -280,6 +280,17 @@ skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32
     return SKEI_OK;
 }
 
+skei_status skei_rotate_adjoint(const skei_plan *plan, const float *y, float *out, int32_t B,
+                                const int32_t *g_deg, int32_t g_stride, skei_stream stream) {
+    if (!plan || !y || !out || !g_deg) return SKEI_ERR_ARG;
+    if (B < 1) return SKEI_ERR_SHAPE;
+    if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    if (y == out) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    SKEI_CUDA(launch_rotate_adj(plan, y, out, B, g_deg, g_stride, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
 skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int32_t B,
                            const int32_t *idx, int32_t m, int32_t idx_stride, void *ws,
                            size_t ws_bytes, skei_stream stream) {
@@ -334,6 +345,63 @@ skei_status skei_fbp(const skei_plan *plan, const float *p, float *x, int32_t B,
     SKEI_CUDA(launch_ramp(plan, p, q, B * m, s));
     AdjJob job{q, x, (float)(M_PI / (2.0 * (double)m_total))};
     SKEI_CUDA(launch_radon_adj(plan, &job, 1, B, idx, m, idx_stride, s));
+    return SKEI_OK;
+}
+
+skei_status skei_ei_grad(const skei_plan *plan, int32_t B, const float *x2, const float *x3,
+                         const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                         int32_t idx_stride, float *grad, void *ws, size_t ws_bytes,
+                         skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x2 || !x3 || !g_deg || !grad || !ws) return SKEI_ERR_ARG;
+    if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    if (grad == x2 || grad == x3) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    const WsLayout wl = ws_layout(plan, B, m);
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
+    // d = 2 (x2 - x3), packed for the forward projector (pack[0..1]) and written (pack[2])
+    float *d = ws_f(ws, wl.pack[2]), *u = ws_f(ws, wl.pack[3]);
+    RotPackJob pj{x2, d, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), ctr, x3, 2.0f};
+    SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
+    // M d = (pi/2m) A_S^T ramp(A_S d); u = d - M d
+    float *p = ws_f(ws, wl.ri);  // A_S d (the interleaved-r region is free outside the pass)
+    FwdJob fj{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), p, nullptr, nullptr};
+    const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
+    SKEI_CUDA(launch_radon_fwd(plan, &fj, 1, B, idx, m, idx_stride, scr, s));
+    const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
+    float *q = ws_f(ws, wl.q), *qi = il ? ws_f(ws, wl.qi) : nullptr;
+    SKEI_CUDA(launch_ramp(plan, p, q, B * m, s, qi, m, 4));
+    AdjJob aj{q, u, (float)(-M_PI / (2.0 * (double)m)), qi, d};
+    SKEI_CUDA(launch_radon_adj(plan, &aj, 1, B, idx, m, idx_stride, s));
+    // grad = T_g^T u
+    SKEI_CUDA(launch_rotate_adj(plan, u, grad, B, g_deg, g_stride, s));
+    return SKEI_OK;
+}
+
+skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, int32_t B,
+                             const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
+                             void *ws, size_t ws_bytes, skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!x || !p || !ws) return SKEI_ERR_ARG;
+    if (m_total < m) return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    const WsLayout w = ws_layout(plan, B, m);
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
+    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+    SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
+    float *ax = ws_f(ws, w.q);  // A_S x
+    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ax, nullptr, nullptr};
+    const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
+    SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, scr, s));
+    // p = (pi / 2 m_total) ramp(A_S x): the scale folded into the ramp's spectrum
+    SKEI_CUDA(launch_ramp(plan, ax, p, B * m, s, nullptr, 0, 0, nullptr, nullptr,
+                          (float)(M_PI / (2.0 * (double)m_total))));
     return SKEI_OK;
 }
 

@@ -54,6 +54,8 @@ struct RotPackJob {
     int g_stride;        // 0 shared, 1 per image
     float *xr, *xc;      // row- / col-packed outputs or NULL
     unsigned *zero;      // if set, block (0,0,0) zeroes zero[0..kPassCounters) (pass counters)
+    const float *xm = nullptr;  // identity job only: pack (and write) ascale * (x - xm)
+    float ascale = 1.f;
 };
 // Pass counters: [0] MC completion, [1] EI completion, [2..] the forward's stream-K split-unit
 // piece counters (one per cluster, <= 256 SMs).
@@ -67,6 +69,9 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
                                int bb, cudaStream_t s);
 cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
                           const int32_t *g, int g_stride, cudaStream_t s);
+// out = T_g^T y (gather form of the rotation's transpose)
+cudaError_t launch_rotate_adj(const skei_plan *plan, const float *y, float *out, int B,
+                              const int32_t *g, int g_stride, cudaStream_t s);
 
 // Forward projector on packed input; up to two jobs (e.g. A_S x1 and A_S x2) per launch.
 // Job 0 may fuse the MC residual: y != NULL -> r = p - y_S (if r != NULL) and mc = sum r^2.
@@ -102,7 +107,14 @@ inline size_t adj_il_floats(const skei_plan *plan, int B, int m) {
     return (size_t)((B + 3) / 4) * m * (plan->n_det + 2 * kAdjPad) * 4;
 }
 // pi: the same sinogram as p in the interleaved layout (or NULL: staged from p)
-struct AdjJob { const float *p; float *x; float scale; const float *pi = nullptr; };
+// base: if set, x = base + scale A^T p (same layout as x)
+struct AdjJob {
+    const float *p;
+    float *x;
+    float scale;
+    const float *pi = nullptr;
+    const float *base = nullptr;
+};
 struct AdjEi {
     const float *x2;  // [B][n][n]
     float *part;      // [B][adj_ei_part_floats / B]
@@ -117,7 +129,7 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi = nullptr, int m = 0, int bb = 0,
-                        const float *rs = nullptr, float *ri = nullptr);
+                        const float *rs = nullptr, float *ri = nullptr, float rscale = 1.f);
 
 // Residual: partials in ws (float2 per (image, chunk)), then final reduce.
 size_t residual_ws_bytes(const skei_plan *plan, int B, int m);

@@ -279,7 +279,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
                 const long o = (long)(b0 + b) * nn + (long)r * n + c;
-                const float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
+                float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
+                if (a.job[jj].base) {  // x = base + scale A^T p
+                    if (c < n) v0 += __ldg(a.job[jj].base + o);
+                    if (c + 1 < n) v1 += __ldg(a.job[jj].base + o + 1);
+                }
                 if (c + 1 < n && ((o & 1) == 0)) {
                     *reinterpret_cast<float2 *>(a.job[jj].x + o) = make_float2(v0, v1);
                 } else {

@@ -86,6 +86,7 @@ struct RampArgs {
     float *q;
     int rows, n_det, P;
     const float *R;    // [P] spectrum / P
+    float rscale;      // output scale (folded into the spectrum as it is applied; 1 = none)
     const float2 *tw;  // per-pass twiddle tables [k][r], k < Ns, r < R
     int npass;
     // optional interleaved copy for the backprojector's bulk window copies:
@@ -129,7 +130,7 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
             } else {
                 v[jj][r] = z[pad(i)];
                 if (mode & kScale) {
-                    const float s = __ldg(a.R + i);
+                    const float s = __ldg(a.R + i) * a.rscale;
                     v[jj][r].x *= s;
                     v[jj][r].y *= s;
                 }
@@ -243,7 +244,8 @@ void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal) 
 }
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
-                        cudaStream_t s, float *qi, int m, int bb, const float *rs, float *ri) {
+                        cudaStream_t s, float *qi, int m, int bb, const float *rs, float *ri,
+                        float rscale) {
     RampArgs a;
     a.rs = rs;
     a.ri = ri;
@@ -257,6 +259,7 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     a.n_det = plan->n_det;
     a.P = plan->fft_len;
     a.R = plan->d_ramp;
+    a.rscale = rscale;
     a.tw = plan->d_twp;
     a.npass = plan->fft_npass;
     const int RL = plan->fft_radix[plan->fft_npass - 1];

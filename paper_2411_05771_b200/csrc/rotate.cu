@@ -34,7 +34,9 @@ template <> struct VecT<1> { using T = float; };
 template <> struct VecT<2> { using T = float2; };
 template <> struct VecT<4> { using T = float4; };
 
-template <int BB>
+// XM: the identity job packs ascale * (x - xm) (a separate instantiation, so the pass's
+// rotation + packing is compiled without it)
+template <int BB, bool XM>
 __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     constexpr int R = 32 / BB;
     using V = typename VecT<BB>::T;
@@ -75,6 +77,12 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
 #pragma unroll
                 for (int b = 0; b < BB; ++b)
                     if (b0 + b < a.B) v[b] = __ldg(job.x + (b0 + b) * nn + (long)r * n + c);
+                if (XM && job.xm) {  // d = ascale (x - xm) (the EI gradient's 2 (x2 - x3))
+#pragma unroll
+                    for (int b = 0; b < BB; ++b)
+                        if (b0 + b < a.B)
+                            v[b] = job.ascale * (v[b] - __ldg(job.xm + (b0 + b) * nn + (long)r * n + c));
+                }
             } else {
                 // split-precision source coordinates: the tile origin's source position
                 // (fp64, sRot) plus an fp32 offset of at most 2 x 32 pixels
@@ -143,7 +151,90 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     }
 }
 
+// k_rotate_adj: out = T_g^T y, the transpose of the rotation, as a
+// GATHER (no atomics): input pixel p = (rp, cp) receives w * y[o] from every output pixel
+// o whose source position (r', c') has p among its 4 bilinear neighbours, with w the
+// bilinear weight o gives p.  Those o lie in the image of the square |r' - rp| < 1,
+// |c' - cp| < 1 under the inverse rotation, whose bounding box has half-width
+// |cos g| + |sin g| <= sqrt 2: a 4 x 4 candidate window around p's inverse image.  Each
+// candidate's source position is formed in fp64 (as the oracle's definition) and the
+// weight is nonzero only if p is one of its neighbours.  One thread per pixel and 4 rows,
+// the BB images of a group share the weights when g is shared.
+template <int BB>
+__global__ void __launch_bounds__(kThreads) k_rotate_adj(const float *y, float *out, int n, int B,
+                                                         const int32_t *g, int g_stride,
+                                                         const double2 *rot, int tiles_c) {
+    const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
+    const int r0 = blockIdx.x / tiles_c * kT, c0 = blockIdx.x % tiles_c * kT;
+    const int b0 = blockIdx.y * BB;
+    const long nn = (long)n * n;
+    const double h = (n - 1) * 0.5;
+    const int c = c0 + tc;
+    const int nimg = g_stride ? 1 : BB;  // images sharing one rotation per weight pass
+#pragma unroll 1
+    for (int bs = 0; bs < BB; bs += nimg) {
+        if (b0 + bs >= B) break;
+        const int gd = g[g_stride ? b0 + bs : 0];
+        const double2 csg = rot[((gd % 360) + 360) % 360];  // exact at multiples of 90
+        const double cg = csg.x, sg = csg.y;
+        const double wbox = fabs(cg) + fabs(sg);
+#pragma unroll 1
+        for (int i = 0; i < kT / 8; ++i) {
+            const int r = r0 + tr + 8 * i;
+            if (r >= n || c >= n) continue;
+            // inverse image of p's centre: u_o = u' cos - v' sin, v_o = u' sin + v' cos
+            const double up = c - h, vp = h - r;
+            const double uo = up * cg - vp * sg, vo = up * sg + vp * cg;
+            const int ocmin = (int)floor(uo + h - wbox), ormin = (int)floor(h - vo - wbox);
+            float acc[BB];
+#pragma unroll
+            for (int b = 0; b < BB; ++b) acc[b] = 0.f;
+#pragma unroll
+            for (int dr = 0; dr < 4; ++dr) {
+                const int ro = ormin + dr;
+                if (ro < 0 || ro >= n) continue;
+#pragma unroll
+                for (int dc = 0; dc < 4; ++dc) {
+                    const int co = ocmin + dc;
+                    if (co < 0 || co >= n) continue;
+                    // source position of output pixel (ro, co), as in the forward definition
+                    const double u = co - h, v = h - ro;
+                    const double us = u * cg + v * sg, vs = -u * sg + v * cg;
+                    const double cs = us + h, rs = h - vs;
+                    const double fr = floor(rs), fc = floor(cs);
+                    const int er = r - (int)fr, ec = c - (int)fc;  // p relative to (floor r', floor c')
+                    if (er < 0 || er > 1 || ec < 0 || ec > 1) continue;
+                    const double a = rs - fr, bb = cs - fc;
+                    const float w = (float)((er ? a : 1.0 - a) * (ec ? bb : 1.0 - bb));
+                    const long oo = (long)ro * n + co;
+#pragma unroll
+                    for (int b = 0; b < BB; ++b)
+                        if (b < nimg && b0 + bs + b < B)
+                            acc[b] = fmaf(w, __ldg(y + (b0 + bs + b) * nn + oo), acc[b]);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < BB; ++b)
+                if (b < nimg && b0 + bs + b < B) out[(b0 + bs + b) * nn + (long)r * n + c] = acc[b];
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_rotate_adj(const skei_plan *plan, const float *y, float *out, int B,
+                              const int32_t *g, int g_stride, cudaStream_t s) {
+    const int n = plan->n;
+    const int tiles_c = (n + kT - 1) / kT;
+    const int bb = g_stride ? 1 : (B % 4 == 0 ? 4 : (B % 2 == 0 ? 2 : 1));
+    dim3 grid((unsigned)(tiles_c * tiles_c), (unsigned)((B + bb - 1) / bb), 1);
+    switch (bb) {
+        case 4: k_rotate_adj<4><<<grid, kThreads, 0, s>>>(y, out, n, B, g, g_stride, plan->d_rot, tiles_c); break;
+        case 2: k_rotate_adj<2><<<grid, kThreads, 0, s>>>(y, out, n, B, g, g_stride, plan->d_rot, tiles_c); break;
+        default: k_rotate_adj<1><<<grid, kThreads, 0, s>>>(y, out, n, B, g, g_stride, plan->d_rot, tiles_c); break;
+    }
+    return cudaGetLastError();
+}
 
 size_t pack_floats(const skei_plan *plan, int B, int bb) {
     const int R = 32 / bb;
@@ -165,11 +256,20 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
     const int side = a.nblk * R > plan->n ? a.nblk * R : plan->n;
     a.tiles_c = (side + kT - 1) / kT;
     dim3 grid((unsigned)(a.tiles_c * a.tiles_c), (unsigned)((B + bb - 1) / bb), (unsigned)njobs);
+    const bool xm = a.job[0].xm || (njobs > 1 && a.job[1].xm);
+#define SKEI_ROTPACK(BBV)                                                       \
+    do {                                                                        \
+        if (xm)                                                                 \
+            k_rotate_pack<BBV, true><<<grid, kThreads, 0, s>>>(a);              \
+        else                                                                    \
+            k_rotate_pack<BBV, false><<<grid, kThreads, 0, s>>>(a);             \
+    } while (0)
     switch (bb) {
-        case 4: k_rotate_pack<4><<<grid, kThreads, 0, s>>>(a); break;
-        case 2: k_rotate_pack<2><<<grid, kThreads, 0, s>>>(a); break;
-        default: k_rotate_pack<1><<<grid, kThreads, 0, s>>>(a); break;
+        case 4: SKEI_ROTPACK(4); break;
+        case 2: SKEI_ROTPACK(2); break;
+        default: SKEI_ROTPACK(1); break;
     }
+#undef SKEI_ROTPACK
     return cudaGetLastError();
 }
 
