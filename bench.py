@@ -53,6 +53,9 @@ def parse():
                          "angle: one batch, the sketch's angles split over the ranks with one "
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
                          "BASELINE cfg5)")
+    ap.add_argument("--path", default="pass", choices=["pass", "ei-grad"],
+                    help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
+                         "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -253,10 +256,88 @@ def run_angle(args):
     return 0
 
 
+def run_ei_grad(args):
+    """--path ei-grad (one GPU): skei_ei_grad on a cfg3 batch whose x2 and
+    x_fbp come from one pass; one CUDA graph per step (5 launches), L2 flushed before every
+    timed step, CUDA events.  The oracle (oracle.ei_grad, fp64, 1 core) is timed on a
+    bounded sample of images."""
+    import torch
+
+    import paper_2411_05771_b200 as sk
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    B, m, N = cfg.B, cfg.m, cfg.N
+    plan = sk.Plan.get(N, cfg.n_det, cfg.n_full, cfg.fft_len, device=0)
+    x1_np, y_np = synth.make_workload(cfg, args.seed)
+    x1, y = torch.from_numpy(x1_np).to(dev), torch.from_numpy(y_np).to(dev)
+    g, idx = sk.draw_device(args.seed, 0, 0, 1, True, cfg.n_full, m)
+    out = sk.sketched_pass(plan, x1, y, g, idx)
+    ws = plan.workspace(B, m)
+    grad = torch.empty_like(x1)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    cap = torch.cuda.Stream(dev)
+    gr = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(gr, stream=cap):
+        sk.ei_grad(plan, out["x2"], out["xfbp"], g, idx, out=grad, ws=ws)
+    for _ in range(args.warmup):
+        gr.replay()
+    torch.cuda.synchronize()
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    recs = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = mk(), mk()
+            a.record(stream)
+            gr.replay()
+            b.record(stream)
+            recs.append((a, b))
+        torch.cuda.synchronize()
+    ms = float(sum(a.elapsed_time(b) for a, b in recs))
+    import oracle
+    og, oidx = int(g[0]), idx[0].cpu().numpy()
+    t0, n_img = time.perf_counter(), 0
+    while time.perf_counter() - t0 < min(args.cpu_seconds, 20.0) or n_img == 0:
+        oracle.ei_grad(x1_np[n_img % B], og, oidx, cfg.n_full, cfg.n_det)
+        n_img += 1
+    cpu_s = time.perf_counter() - t0
+    taps = B * (4 * N * N + 4 * m * N * N)  # T^T 4/px; A_S d and A_S^T q: 2 taps per (px, angle)
+    props = torch.cuda.get_device_properties(dev)
+    peak_gbs = props.multi_processor_count * 128 * (clk.summary()["sm_max_mhz"] or 1965) * 1e6 / 1e9
+    line = {
+        "metric": f"EI-branch gradients/s (batches of {B}) at {N}², {cfg.n_full}→{m} angles",
+        "value": args.steps / (ms * 1e-3), "unit": "gradients/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {**workload_desc(cfg, args.mode),
+                                        "launch": "one CUDA graph per step (5 launches)",
+                                        "path": "skei_ei_grad (SURVEY 8(f) #1)"},
+        "roofline": {"bound": "smem", "unit": "GB/s", "taps_per_step": taps,
+                     "achieved": 4 * taps * args.steps / (ms * 1e-3) / 1e9,
+                     "peak": peak_gbs, "frac": 4 * taps * args.steps / (ms * 1e-3) / 1e9 / peak_gbs,
+                     "algorithmic": "4 B per tap; T_g^T 4 taps/px, A_S d and A_S^T q 2 taps per "
+                                    "(px, angle)",
+                     "peak_source": "148 SMs x 128 B/clk x SM max clock (theoretical shared-memory "
+                                    "bandwidth; the pass bench's live probe measures 99.6% of it)"},
+        "cpu_baseline": {"value": (n_img / B) / cpu_s, "unit": "gradients/s", "cores": 1,
+                         "kind": "oracle", "sample": f"{n_img} image(s) through oracle.ei_grad "
+                                                     f"({cpu_s:.1f} s; {B} images = 1 gradient)"},
+        "gpu_launches": 5 * args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.path == "ei-grad":
+        return run_ei_grad(args)
     if args.split == "angle":
         if args.config == "cfg3" and "--config" not in sys.argv:
             args.config = "cfg5"
