@@ -48,11 +48,12 @@ def parse():
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
     ap.add_argument("--mode", default="uniform", choices=["uniform", "interleaved"])
-    ap.add_argument("--split", default="batch", choices=["batch", "angle"],
+    ap.add_argument("--split", default="batch", choices=["batch", "angle", "angle-ag"],
                     help="batch: every rank runs its own batch (weak scaling, no collective); "
                          "angle: one batch, the sketch's angles split over the ranks with one "
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
-                         "BASELINE cfg5)")
+                         "BASELINE cfg5); angle-ag: the same split exchanging filtered "
+                         "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2)")
     ap.add_argument("--path", default="pass", choices=["pass", "ei-grad"],
                     help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
                          "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad)")
@@ -213,9 +214,11 @@ def run_angle(args):
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    split_fn = skdist.angle_split_pass_allgather if args.split == "angle-ag" else skdist.angle_split_pass
+
     def step(it):
         g, idx = sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, cfg.m, mode)
-        return skdist.angle_split_pass(ops, x1, y, g, idx[0])
+        return split_fn(ops, x1, y, g, idx[0])
 
     for i in range(args.warmup):
         step(i)
@@ -245,9 +248,13 @@ def run_angle(args):
             "unit": "passes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {**workload_desc(cfg, args.mode), "parallelism": f"angle split x{world}",
-                       "allreduce_bytes": int(out["allreduce_bytes"]),
-                       "launch": "direct (not graphed): 8 library calls + 1 NCCL all-reduce"},
+            "config": {**workload_desc(cfg, args.mode),
+                       "parallelism": f"angle split x{world}" + (" (all-gather of filtered rows, "
+                                                                   "row-band backprojection)"
+                                                                   if args.split == "angle-ag" else ""),
+                       **({"allgather_bytes": int(out["allgather_bytes"])} if args.split == "angle-ag"
+                          else {"allreduce_bytes": int(out["allreduce_bytes"])}),
+                       "launch": "direct (not graphed): library calls + NCCL collectives"},
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -338,7 +345,7 @@ def main():
         return run_reference(args)
     if args.path == "ei-grad":
         return run_ei_grad(args)
-    if args.split == "angle":
+    if args.split in ("angle", "angle-ag"):
         if args.config == "cfg3" and "--config" not in sys.argv:
             args.config = "cfg5"
         return run_angle(args)

@@ -143,6 +143,23 @@ skei_status skei_rotate_adjoint(const skei_plan *plan, const float *y, float *ou
  * grad: [B][n][n] device, must not alias x2 or x3; ws >= skei_workspace_bytes(plan, B, m).
  * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL, strides,
  * aliasing, ws too small). */
+/* ---------------- next row: communication-reduced single-image split --
+ * The backprojections of the pass restricted to output rows [row0, row0 + rows): with q
+ * (the filtered sinogram) and r (the residual) of ALL m sketched angles at hand — after
+ * an all-gather of the ranks' angle shards, 2 B m n_det floats — every rank computes its
+ * own row band of x_fbp = (pi / 2 m_total) A_S^T q and grad = 2 A_S^T r, and the band's
+ * ei partial sum (x2 - x_fbp)^2 (fused, fixed-order reduction), instead of whole-image
+ * partials that need an all-reduce of 2 B n^2 floats.  q, r: [B][m][n_det]; x2: [B][n][n]
+ * (whole images); xfbp_band, grad_band: [B][rows][n]; ei_band: [B]; all device.
+ * Errors: SKEI_ERR_SHAPE (B, m, or the band outside [0, n)), SKEI_ERR_ARG (NULL, strides,
+ * m_total < m, ws too small). */
+skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float *q,
+                                  const float *r, const int32_t *idx, int32_t m,
+                                  int32_t idx_stride, int32_t m_total, const float *x2,
+                                  int32_t row0, int32_t rows, float *xfbp_band,
+                                  float *grad_band, float *ei_band, void *ws, size_t ws_bytes,
+                                  skei_stream stream);
+
 /* The transpose of skei_fbp (next row): p = (pi / 2 m_total) ramp(A_S x)
  * (the ramp kernel is even, so ramp is symmetric), i.e. the vector-Jacobian product of
  * the sketched FBP.  x: [B][n][n], p: [B][m][n_det] device; other arguments and errors as

@@ -79,6 +79,8 @@ def lib():
             "skei_rotate_adjoint": ([vp, vp, vp, i32, vp, i32, vp], st),
             "skei_ei_grad": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, vp, sz, vp], st),
             "skei_fbp_adjoint": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
+            "skei_backproject_band": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp,
+                                       vp, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
             "skei_radon_adj": ([vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, vp], st),
             "skei_ramp_filter": ([vp, vp, vp, i32, vp], st),
@@ -239,6 +241,25 @@ def fbp_adjoint(plan: Plan, x: torch.Tensor, idx: torch.Tensor, m_total: int | N
                                   int(m_total or m), _ptr(ws, torch.uint8, "ws"), ws.numel(),
                                   _stream(x)), "skei_fbp_adjoint")
     return p
+
+
+def backproject_band(plan: Plan, q: torch.Tensor, r: torch.Tensor, idx: torch.Tensor,
+                     x2: torch.Tensor, row0: int, rows: int, m_total: int | None = None,
+                     ws: torch.Tensor | None = None):
+    """skei_backproject_band: (x_fbp band, grad band, ei band partial) for output rows
+    [row0, row0 + rows) from the whole filtered sinogram q and residual r."""
+    B, m = q.shape[0], idx.shape[-1]
+    xf = torch.empty(B, rows, plan.n, dtype=torch.float32, device=q.device)
+    gr = torch.empty_like(xf)
+    ei = torch.empty(B, dtype=torch.float32, device=q.device)
+    ws = plan.workspace(B, m) if ws is None else ws
+    _check(lib().skei_backproject_band(plan.handle, B, _ptr(q, name="q"), _ptr(r, name="r"),
+                                       _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                                       int(m_total or m), _ptr(x2, name="x2"), int(row0),
+                                       int(rows), _ptr(xf, name="xfbp"), _ptr(gr, name="grad"),
+                                       _ptr(ei, name="ei"), _ptr(ws, torch.uint8, "ws"),
+                                       ws.numel(), _stream(q)), "skei_backproject_band")
+    return xf, gr, ei
 
 
 def ei_grad(plan: Plan, x2: torch.Tensor, x3: torch.Tensor, g: torch.Tensor, idx: torch.Tensor,

@@ -381,6 +381,29 @@ skei_status skei_ei_grad(const skei_plan *plan, int32_t B, const float *x2, cons
     return SKEI_OK;
 }
 
+skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float *q,
+                                  const float *r, const int32_t *idx, int32_t m,
+                                  int32_t idx_stride, int32_t m_total, const float *x2,
+                                  int32_t row0, int32_t rows, float *xfbp_band,
+                                  float *grad_band, float *ei_band, void *ws, size_t ws_bytes,
+                                  skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!q || !r || !x2 || !xfbp_band || !grad_band || !ei_band || !ws) return SKEI_ERR_ARG;
+    if (m_total < m) return SKEI_ERR_ARG;
+    if (row0 < 0 || rows < 1 || row0 + rows > plan->n) return SKEI_ERR_SHAPE;
+    if (ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    const WsLayout wl = ws_layout(plan, B, m);
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
+    SKEI_CUDA(cudaMemsetAsync(ctr + 1, 0, sizeof(unsigned), s));  // the ei completion counter
+    AdjJob aj[2] = {{q, xfbp_band, (float)(M_PI / (2.0 * (double)m_total))}, {r, grad_band, 2.0f}};
+    AdjEi eif{x2, ws_f(ws, wl.eipart), ctr + 1, ei_band};
+    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, &eif, row0, rows));
+    return SKEI_OK;
+}
+
 skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, int32_t B,
                              const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
                              void *ws, size_t ws_bytes, skei_stream stream) {

@@ -122,9 +122,11 @@ struct AdjEi {
     float *out;       // ei [B]
 };
 size_t adj_ei_part_floats(const skei_plan *plan, int B);
+// row0, rows: backproject only output rows [row0, row0 + rows) into [B][rows][n] outputs
+// (rows < 0: whole images)
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
-                             const AdjEi *ei = nullptr);
+                             const AdjEi *ei = nullptr, int row0 = 0, int rows = -1);
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,

@@ -41,6 +41,8 @@ struct AdjArgs {
     AdjJob job[2];
     const int32_t *idx;
     int m, idx_stride, B, tiles_x, tiles_y;
+    int row0, row1;  // output rows [row0, row1) (a row band; [0, n) for whole images); the
+                     // outputs (and base) are [B][row1 - row0][n], x2 of the fused ei [B][n][n]
     Geom g;
     // fused ei epilogue (job 0 = FBP): x2 [B][n][n], partials [B][ntiles], counter, ei [B]
     const float *ei_x2;
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
-    const int tr0 = (tile / a.tiles_x) * kTileH, tc0 = (tile % a.tiles_x) * kTileW;
+    const int tr0 = a.row0 + (tile / a.tiles_x) * kTileH, tc0 = (tile % a.tiles_x) * kTileW;
     const int b0 = blockIdx.y * BB;
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -275,20 +277,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) {
             const int c = tc0 + 2 * (pc0 + 16 * p);
-            if (r >= n) continue;
+            if (r >= a.row1) continue;
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
-                const long o = (long)(b0 + b) * nn + (long)r * n + c;
+                const long o = (long)(b0 + b) * nn + (long)r * n + c;  // in a whole image
+                const long ox = (long)(b0 + b) * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
                 float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
                 if (a.job[jj].base) {  // x = base + scale A^T p
-                    if (c < n) v0 += __ldg(a.job[jj].base + o);
-                    if (c + 1 < n) v1 += __ldg(a.job[jj].base + o + 1);
+                    if (c < n) v0 += __ldg(a.job[jj].base + ox);
+                    if (c + 1 < n) v1 += __ldg(a.job[jj].base + ox + 1);
                 }
-                if (c + 1 < n && ((o & 1) == 0)) {
-                    *reinterpret_cast<float2 *>(a.job[jj].x + o) = make_float2(v0, v1);
+                if (c + 1 < n && ((ox & 1) == 0)) {
+                    *reinterpret_cast<float2 *>(a.job[jj].x + ox) = make_float2(v0, v1);
                 } else {
-                    if (c < n) a.job[jj].x[o] = v0;
-                    if (c + 1 < n) a.job[jj].x[o + 1] = v1;
+                    if (c < n) a.job[jj].x[ox] = v0;
+                    if (c + 1 < n) a.job[jj].x[ox + 1] = v1;
                 }
                 if (jj == 0 && a.ei_x2) {
                     if (c < n) {
@@ -368,7 +371,7 @@ size_t adj_ei_part_floats(const skei_plan *plan, int B) {
 
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
-                             const AdjEi *ei) {
+                             const AdjEi *ei, int row0, int rows) {
     AdjArgs a;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
@@ -377,8 +380,10 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
     a.idx_stride = idx_stride;
     a.B = B;
     a.g = geom_of(plan);
+    a.row0 = row0 < 0 ? 0 : row0;
+    a.row1 = rows < 0 ? plan->n : a.row0 + rows;
     a.tiles_x = (plan->n + kTileW - 1) / kTileW;
-    a.tiles_y = (plan->n + kTileH - 1) / kTileH;
+    a.tiles_y = (a.row1 - a.row0 + kTileH - 1) / kTileH;
     a.ei_x2 = ei ? ei->x2 : nullptr;
     a.ei_part = ei ? ei->part : nullptr;
     a.ei_ctr = ei ? ei->ctr : nullptr;

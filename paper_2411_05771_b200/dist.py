@@ -31,7 +31,8 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-__all__ = ["batch_range", "angle_shard", "CudaOps", "angle_split_pass", "batch_split_images"]
+__all__ = ["batch_range", "angle_shard", "CudaOps", "angle_split_pass", "batch_split_images",
+           "angle_split_pass_allgather", "shard_phase", "band_phase"]
 
 
 def batch_range(B: int, rank: int, world: int) -> range:
@@ -89,6 +90,14 @@ class CudaOps:
         _, ei, _ = sk.ei_residual(self.plan, None, None, idx, x2, x3)
         return ei
 
+    def ramp(self, p):
+        import paper_2411_05771_b200 as sk
+        return sk.ramp_filter(self.plan, p)
+
+    def backproject_band(self, q, r, idx, x2, row0, rows, m_total):
+        import paper_2411_05771_b200 as sk
+        return sk.backproject_band(self.plan, q, r, idx, x2, row0, rows, m_total=m_total)
+
 
 def angle_split_pass(ops, x1, y, g, idx, group=None):
     """One sketched-EI pass of a batch whose sketch `idx` (m ascending indices) is split over
@@ -133,3 +142,68 @@ def ring_bytes_per_gpu(B: int, N: int, world: int) -> float:
 
 def expected_scale(m_total: int) -> float:
     return math.pi / (2.0 * m_total)
+
+
+# ---------------------------------------------------------------------------------------
+# Communication-reduced single-image split: every rank projects and
+# filters its angle shard, the ranks all-gather the filtered rows q and the residual rows r
+# (2 B m n_det floats in total, 1.48 MB each at cfg5), and every rank backprojects ALL the
+# angles for its own row band of the image (skei_backproject_band: x_fbp, grad and the
+# band's ei partial).  One all-reduce of 2 B scalars (mc, ei) completes the losses.  Per
+# GPU that moves (G-1)/G x 2.97 MB instead of the 2 (G-1)/G x 8.4 MB of the all-reduce of
+# whole-image partials; the outputs x_fbp and grad stay row-sharded (band r on rank r).
+
+def shard_phase(ops, x1, y, g, idx, rank: int, world: int):
+    """Before the exchange: x2 (replicated), this rank's angle shard, its filtered rows
+    q and residual rows r, and its mc partial."""
+    sub = angle_shard(idx, rank, world)
+    x2 = ops.rotate(x1, g)
+    p1 = ops.forward(x1, sub)
+    p2 = ops.forward(x2, sub)
+    mc_part, r = ops.residual(p1, y, sub)
+    return {"x2": x2, "idx": sub, "q": ops.ramp(p2), "r": r, "mc": mc_part}
+
+
+def band_phase(ops, q_full, r_full, idx, x2, rank: int, world: int):
+    """After the exchange: this rank's row band of x_fbp and grad from all m angles, and the
+    band's ei partial."""
+    N = x2.shape[-1]
+    band = batch_range(N, rank, world)
+    xf, gr, ei = ops.backproject_band(q_full, r_full, idx, x2, band.start, len(band), idx.shape[-1])
+    return {"rows": band, "xfbp": xf, "grad": gr, "ei": ei}
+
+
+def angle_split_pass_allgather(ops, x1, y, g, idx, group=None):
+    """One pass of a batch whose sketch `idx` is split over the ranks of `group`, exchanging
+    filtered sinogram rows instead of partial images (module comment above).  Returns x2,
+    this rank's row bands of x_fbp and grad (`rows`), and the complete mc and ei ([B])."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    sh = shard_phase(ops, x1, y, g, idx, rank, world)
+    B, n_det = sh["q"].shape[0], sh["q"].shape[-1]
+    sizes = [len(batch_range(len(idx), r, world)) for r in range(world)]
+    mx = max(sizes)
+    # equal-sized all-gather buffers: [B][2][mx][n_det] per rank (q rows, r rows), padded
+    send = torch.zeros(B, 2, mx, n_det, dtype=sh["q"].dtype, device=sh["q"].device)
+    send[:, 0, :sh["q"].shape[1]] = sh["q"]
+    send[:, 1, :sh["r"].shape[1]] = sh["r"]
+    if world > 1:
+        recv = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(recv, send, group=group)
+    else:
+        recv = [send]
+    q_full = torch.cat([recv[i][:, 0, :sizes[i]] for i in range(world)], dim=1).contiguous()
+    r_full = torch.cat([recv[i][:, 1, :sizes[i]] for i in range(world)], dim=1).contiguous()
+    bd = band_phase(ops, q_full, r_full, idx, sh["x2"], rank, world)
+    scal = torch.cat([sh["mc"].to(bd["ei"].dtype), bd["ei"]])
+    if world > 1:
+        dist.all_reduce(scal, op=dist.ReduceOp.SUM, group=group)
+    return {"x2": sh["x2"], "xfbp": bd["xfbp"], "grad": bd["grad"], "rows": bd["rows"],
+            "mc": scal[:B], "ei": scal[B:], "idx": sh["idx"],
+            "allgather_bytes": send.numel() * send.element_size() * world}
+
+
+def allgather_bytes(B: int, m: int, n_det: int) -> int:
+    """Bytes all ranks contribute to the exchange of the all-gather split: 2 B m n_det fp32."""
+    return 4 * 2 * B * m * n_det
+

@@ -76,3 +76,43 @@ def test_angle_split_pass_single_rank_equals_pass():
     full = sk.sketched_pass(plan, x1, y, g, idx)
     for k in ("x2", "xfbp", "grad", "mc", "ei"):
         _close(out[k], full[k], k)
+
+
+@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 3), ("cfg5", 4), ("cfg5", 8)])
+def test_allgather_split_bands_tile_full_pass(name, world):
+    """SURVEY §8(f) #2 (a) simulated on one GPU: every 'rank' projects, filters and computes
+    the residual of its angle shard (shard_phase); the shards' q and r rows, concatenated in
+    rank order (what the all-gather delivers), are backprojected by every rank for its row
+    band (band_phase, skei_backproject_band).  The bands tile x_fbp and grad of the
+    single-GPU pass; the mc and ei partials sum to its mc and ei."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    ops = skdist.CudaOps(plan)
+    idx_h = idx[0].cpu()
+    shards = [skdist.shard_phase(ops, x1, y, g, idx_h.cuda(), r, world) for r in range(world)]
+    q = torch.cat([s["q"] for s in shards], dim=1).contiguous()
+    r = torch.cat([s["r"] for s in shards], dim=1).contiguous()
+    bands = [skdist.band_phase(ops, q, r, idx, shards[0]["x2"], rk, world) for rk in range(world)]
+    assert [b["rows"].start for b in bands] == sorted(b["rows"].start for b in bands)
+    _close(torch.cat([b["xfbp"] for b in bands], dim=1), full["xfbp"], "xfbp bands")
+    _close(torch.cat([b["grad"] for b in bands], dim=1), full["grad"], "grad bands")
+    _close(sum(s["mc"] for s in shards), full["mc"], "mc")
+    _close(sum(b["ei"] for b in bands), full["ei"], "ei")
+
+
+def test_allgather_split_single_rank_equals_pass():
+    cfg = synth.CONFIGS["cfg1"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    out = skdist.angle_split_pass_allgather(skdist.CudaOps(plan), x1, y, g, idx[0])
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    for k in ("x2", "xfbp", "grad", "mc", "ei"):
+        _close(out[k], full[k], k)
