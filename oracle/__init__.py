@@ -51,6 +51,10 @@ def _load():
         lib.oracle_draw.argtypes = [u64, u64, u64, i32, i32, i32, ip, ip]
         lib.oracle_rotate.argtypes = [dp, dp, i32, i32]
         lib.oracle_rotate_adj.argtypes = [dp, dp, i32, i32]
+        lib.oracle_rei_noise.argtypes = [u64, u64, u64, i32, i32, dp]
+        lib.oracle_pass_rei.argtypes = [dp, dp, i32, i32, i32, i32, ip, i32, ctypes.c_double,
+                                        u64, u64, u64, dp, dp, dp, dp, dp, dp, dp,
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         lib.oracle_ei_grad.argtypes = [dp, i32, i32, i32, i32, ip, i32, dp]
         lib.oracle_fwd.argtypes = [dp, dp, i32, i32, i32, ip, i32]
         lib.oracle_adj.argtypes = [dp, dp, i32, i32, i32, ip, i32, ctypes.c_double]
@@ -198,3 +202,29 @@ def sketched_pass(x1, y, g: int, idx, n_full: int, x3=None):
                         ctypes.byref(mc), ctypes.byref(ei))
     out["mc"], out["ei"] = mc.value, ei.value
     return out
+
+
+def rei_noise(seed: int, it: int, image: int, m: int, n_det: int):
+    """eps [m][n_det] ~ N(0,1) of the REI pass (oracle.c oracle_rei_noise)."""
+    out = np.empty((m, n_det))
+    _load().oracle_rei_noise(seed, it, image, m, n_det, _dp(out))
+    return out
+
+
+def sketched_pass_rei(x1, y, g: int, idx, n_full: int, sigma: float, seed: int, it: int,
+                      image: int):
+    """The REI pass for one image (oracle.c oracle_pass_rei): q = ramp(p2 + sigma eps)."""
+    x1, y, idx = _d(x1), _d(y), _i(idx)
+    N = x1.shape[-1]
+    n_det = y.shape[-1]
+    m = len(idx)
+    out = {k: np.empty((N, N)) for k in ("x2", "xfbp", "grad")}
+    out.update({k: np.empty((m, n_det)) for k in ("p1", "p2", "q", "r")})
+    mc, ei = ctypes.c_double(0), ctypes.c_double(0)
+    _load().oracle_pass_rei(_dp(x1), _dp(y), N, n_det, n_full, int(g), _ip(idx), m, float(sigma),
+                            seed, it, image, _dp(out["x2"]), _dp(out["p1"]), _dp(out["p2"]),
+                            _dp(out["q"]), _dp(out["xfbp"]), _dp(out["r"]), _dp(out["grad"]),
+                            ctypes.byref(mc), ctypes.byref(ei))
+    out["mc"], out["ei"] = mc.value, ei.value
+    return out
+

@@ -304,10 +304,59 @@ void oracle_residual(const double *p1, const double *y, const int *idx, int m, i
  *   r = p1 - y_S; mc = ||r||^2; ei = ||x2 - x3||^2; grad = 2 A_S^T r.
  * y is the full measured sinogram [n_full][n_det].  Any output pointer may be NULL
  * except those the later steps need internally (allocated here). */
+static void oracle_pass_impl(const double *x1, const double *y, int N, int n_det, int n_full,
+                             int g, const int *idx, int m, const double *x3_in,
+                             const double *p2_noise,
+                             double *x2, double *p1, double *p2, double *q, double *xfbp,
+                             double *r, double *grad, double *mc, double *ei);
+
 void oracle_pass(const double *x1, const double *y, int N, int n_det, int n_full,
                  int g, const int *idx, int m, const double *x3_in,
                  double *x2, double *p1, double *p2, double *q, double *xfbp,
                  double *r, double *grad, double *mc, double *ei)
+{
+    oracle_pass_impl(x1, y, N, n_det, n_full, g, idx, m, x3_in, NULL, x2, p1, p2, q, xfbp, r,
+                     grad, mc, ei);
+}
+
+/* ------------------------------------- REI simulated noise (R23, §8(f) #3) --
+ * eps[k][j] ~ N(0, 1) i.i.d. for sketch row k, bin j of one image: sample s = k n_det + j
+ * is Box-Muller (cos branch) on words 2s and 2s+1 of the counter-based stream keyed by
+ * (seed, stream 5 = REI noise, iter, image), u = ((w >> 11) + 1/2) 2^-53 in (0, 1)
+ * (SURVEY §8(c) O-8's uniform; PAPER.md L104 REI "simulated noise"). */
+void oracle_rei_noise(uint64_t seed, uint64_t iter, uint64_t image, int m, int n_det, double *eps)
+{
+    uint64_t key = oracle_key(seed, 5, iter, image);
+    for (long s = 0; s < (long)m * n_det; ++s) {
+        double u1 = ((double)(oracle_word(key, 2 * (uint64_t)s) >> 11) + 0.5) * 0x1p-53;
+        double u2 = ((double)(oracle_word(key, 2 * (uint64_t)s + 1) >> 11) + 0.5) * 0x1p-53;
+        eps[s] = sqrt(-2.0 * log(u1)) * cos(2.0 * ORACLE_PI * u2);
+    }
+}
+
+/* ------------------------------------------- the REI pass (R23, §8(f) #3) --
+ * The robust-EI variant: the EI branch's reconstruction
+ * sees simulated measurement noise, x3 = F(A_S^+ (A_S x2 + sigma eps)): identical to
+ * oracle_pass except q = ramp(p2 + sigma eps) (p2 itself is reported noise-free). */
+void oracle_pass_rei(const double *x1, const double *y, int N, int n_det, int n_full,
+                     int g, const int *idx, int m, double sigma, uint64_t seed,
+                     uint64_t iter, uint64_t image,
+                     double *x2, double *p1, double *p2, double *q, double *xfbp,
+                     double *r, double *grad, double *mc, double *ei)
+{
+    double *noise = (double *)malloc(sizeof(double) * (size_t)m * (size_t)n_det);
+    oracle_rei_noise(seed, iter, image, m, n_det, noise);
+    for (long s = 0; s < (long)m * n_det; ++s) noise[s] *= sigma;
+    oracle_pass_impl(x1, y, N, n_det, n_full, g, idx, m, NULL, noise, x2, p1, p2, q, xfbp, r,
+                     grad, mc, ei);
+    free(noise);
+}
+
+static void oracle_pass_impl(const double *x1, const double *y, int N, int n_det, int n_full,
+                             int g, const int *idx, int m, const double *x3_in,
+                             const double *p2_noise,
+                             double *x2, double *p1, double *p2, double *q, double *xfbp,
+                             double *r, double *grad, double *mc, double *ei)
 {
     size_t nn = (size_t)N * N, mn = (size_t)m * n_det;
     double *bx2 = x2 ? x2 : (double *)malloc(sizeof(double) * nn);
@@ -321,7 +370,14 @@ void oracle_pass(const double *x1, const double *y, int N, int n_det, int n_full
     oracle_rotate(x1, bx2, N, g);
     oracle_fwd(bx2, bp2, N, n_det, n_full, idx, m);
     oracle_fwd(x1, bp1, N, n_det, n_full, idx, m);
-    oracle_ramp(bp2, bq, m, n_det);
+    if (p2_noise) {  /* REI: the FBP input is p2 + sigma eps */
+        double *pn = (double *)malloc(sizeof(double) * mn);
+        for (size_t s = 0; s < mn; ++s) pn[s] = bp2[s] + p2_noise[s];
+        oracle_ramp(pn, bq, m, n_det);
+        free(pn);
+    } else {
+        oracle_ramp(bp2, bq, m, n_det);
+    }
     oracle_adj(bq, bxf, N, n_det, n_full, idx, m, ORACLE_PI / (2.0 * m));
     oracle_residual(bp1, y, idx, m, n_det, bx2, x3_in ? x3_in : bxf, N, &lmc, &lei, br);
     if (grad) oracle_adj(br, grad, N, n_det, n_full, idx, m, 2.0);

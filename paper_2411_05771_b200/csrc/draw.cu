@@ -7,31 +7,12 @@
 #include <vector>
 
 #include "internal.h"
+#include "sm64.h"
 
 namespace skei {
 namespace {
 
-constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t kStreamRot = 1, kStreamSketch = 2;
-
-__host__ __device__ inline uint64_t sm64_finalize(uint64_t z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    return z ^ (z >> 31);
-}
-
-// i-th output of the SplitMix64 stream whose state starts at `state`.
-__host__ __device__ inline uint64_t sm64_out(uint64_t state, uint64_t i) {
-    return sm64_finalize(state + (i + 1) * kGolden);
-}
-
-__host__ __device__ inline uint64_t sm64_key(uint64_t seed, uint64_t stream, uint64_t iter,
-                                             uint64_t image) {
-    uint64_t k = sm64_out(seed, 0) ^ stream;
-    k = sm64_out(k, 0) ^ iter;
-    k = sm64_out(k, 0) ^ image;
-    return sm64_out(k, 0);
-}
 
 __host__ __device__ inline uint32_t mulhi_below(uint64_t w, uint32_t n) {
 #ifdef __CUDA_ARCH__

@@ -494,3 +494,68 @@ def test_ei_gradient_finite_difference():
         e[r, c] = eps
         fd = (ei(x + e) - ei(x - e)) / (2 * eps)
         assert abs(fd - grad[r, c]) <= 1e-8 * max(1.0, abs(fd))
+
+
+# --------------------------------------------------------- REI variant
+def test_rei_noise_standard_normal_and_independent():
+    """The simulated noise is N(0, 1) (Kolmogorov-Smirnov, 2e5 samples) and differs between
+    images and iterations (near-zero correlation)."""
+    e = oracle.rei_noise(0, 1, 7, 200, 1000).ravel()
+    assert st.kstest(e, "norm").pvalue > 0.01
+    f = oracle.rei_noise(0, 1, 8, 200, 1000).ravel()
+    h = oracle.rei_noise(0, 2, 7, 200, 1000).ravel()
+    assert abs(np.corrcoef(e, f)[0, 1]) < 0.01 and abs(np.corrcoef(e, h)[0, 1]) < 0.01
+
+
+def test_rei_sigma_zero_is_the_plain_pass():
+    cfg = synth.CONFIGS["cfg1"]
+    x1, y = synth.make_workload(cfg, seed=0)
+    g, idx = oracle.draw(0, 0, SH, cfg.n_full, cfg.m)
+    a = oracle.sketched_pass(x1[0], y[0], g, idx, cfg.n_full)
+    b = oracle.sketched_pass_rei(x1[0], y[0], g, idx, cfg.n_full, 0.0, 0, 0, 0)
+    for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["mc"] == b["mc"] and a["ei"] == b["ei"]
+
+
+def test_rei_dense_8x8():
+    """x3_rei = x3 + (pi/2m) A^T H2 (sigma eps) from dense matrices (formula A, closed-form
+    H2) with eps = rei_noise (pinned above)."""
+    N, n_det, n_full, g, sigma = 8, 12, 8, 37, 0.3
+    idx = np.array([1, 2, 5, 7])
+    m = len(idx)
+    A = _dense_A(N, n_det, n_full, idx)
+    lag = np.arange(n_det)[:, None] - np.arange(n_det)[None, :]
+    H = np.where(lag == 0, 0.5, np.where(lag % 2 == 0, 0.0,
+                                         -2 / (np.pi ** 2 * np.maximum(np.abs(lag), 1) ** 2)))
+    Ap = (np.pi / (2 * m)) * A.T @ np.kron(np.eye(m), H)
+    rng = np.random.default_rng(4)
+    x1 = rng.standard_normal((N, N))
+    y = rng.standard_normal((n_full, n_det))
+    plain = oracle.sketched_pass(x1, y, g, idx, n_full)
+    rei = oracle.sketched_pass_rei(x1, y, g, idx, n_full, sigma, 3, 4, 5)
+    eps = oracle.rei_noise(3, 4, 5, m, n_det).ravel()
+    ref = plain["xfbp"].ravel() + Ap @ (sigma * eps)
+    assert np.max(np.abs(rei["xfbp"].ravel() - ref)) < 1e-12
+    assert np.array_equal(rei["p2"], plain["p2"])  # p2 is reported noise-free
+
+
+def test_rei_monte_carlo_noise_inflation():
+    """E ||x3_rei - x3||^2 = sigma^2 ||A_S^+||_F^2 (dense A_S^+ on 8x8); the
+    Monte-Carlo mean over 400 noise draws lies within 4 standard errors."""
+    N, n_det, n_full, g, sigma = 8, 12, 8, 37, 0.5
+    idx = np.array([0, 3, 4, 6])
+    m = len(idx)
+    A = _dense_A(N, n_det, n_full, idx)
+    lag = np.arange(n_det)[:, None] - np.arange(n_det)[None, :]
+    H = np.where(lag == 0, 0.5, np.where(lag % 2 == 0, 0.0,
+                                         -2 / (np.pi ** 2 * np.maximum(np.abs(lag), 1) ** 2)))
+    Ap = (np.pi / (2 * m)) * A.T @ np.kron(np.eye(m), H)
+    expect = sigma ** 2 * float(np.sum(Ap ** 2))
+    rng = np.random.default_rng(5)
+    x1 = rng.standard_normal((N, N))
+    y = rng.standard_normal((n_full, n_det))
+    plain = oracle.sketched_pass(x1, y, g, idx, n_full)["xfbp"]
+    d = np.array([np.sum((oracle.sketched_pass_rei(x1, y, g, idx, n_full, sigma, 0, it, 0)["xfbp"]
+                          - plain) ** 2) for it in range(400)])
+    assert abs(d.mean() - expect) <= 4 * d.std(ddof=1) / np.sqrt(len(d))
