@@ -54,9 +54,10 @@ def parse():
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
                          "BASELINE cfg5); angle-ag: the same split exchanging filtered "
                          "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2)")
-    ap.add_argument("--path", default="pass", choices=["pass", "ei-grad"],
+    ap.add_argument("--path", default="pass", choices=["pass", "ei-grad", "rei"],
                     help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
-                         "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad)")
+                         "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad); "
+                         "rei: the REI pass, q = ramp(p2 + sigma eps) (skei_pass_rei)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -339,12 +340,86 @@ def run_ei_grad(args):
     return 0
 
 
+def run_rei(args):
+    """--path rei (one GPU): skei_pass_rei on the cfg3 batch, sigma = 0.005
+    max|y| (the config's noise level), fresh draw and noise stream every step (graphed per
+    step: draw + 6 launches), L2 flushed before every timed step, CUDA events; oracle REI
+    pass timed beside it on a bounded sample."""
+    import torch
+
+    import paper_2411_05771_b200 as sk
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    B, m = cfg.B, cfg.m
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len, device=0)
+    x1_np, y_np = synth.make_workload(cfg, args.seed)
+    x1, y = torch.from_numpy(x1_np).to(dev), torch.from_numpy(y_np).to(dev)
+    sigma = cfg.noise * float(np.abs(y_np).max())
+    out = sk.alloc_pass_outputs(plan, B, m, dev)
+    ws = plan.workspace(B, m)
+    gbuf = torch.empty(1, dtype=torch.int32, device=dev)
+    ibuf = torch.empty(1, m, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    cap = torch.cuda.Stream(dev)
+    n = args.warmup + args.steps
+    graphs = []
+    torch.cuda.synchronize()
+    for it in range(n):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cap):
+            sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, m, sk.MODE_UNIFORM, g=gbuf, idx=ibuf)
+            sk.sketched_pass_rei(plan, x1, y, gbuf, ibuf, sigma, args.seed, it, 0, out=out, ws=ws)
+        graphs.append(gr)
+    for i in range(args.warmup):
+        graphs[i].replay()
+    torch.cuda.synchronize()
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    recs = []
+    with ClockSampler(0) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = mk(), mk()
+            a.record(stream)
+            graphs[args.warmup + i].replay()
+            b.record(stream)
+            recs.append((a, b))
+        torch.cuda.synchronize()
+    ms = float(sum(a.elapsed_time(b) for a, b in recs))
+    import oracle
+    og, oidx = oracle.draw(args.seed, 0, oracle.SHARED_IMAGE, cfg.n_full, m)
+    t0, n_img = time.perf_counter(), 0
+    while time.perf_counter() - t0 < min(args.cpu_seconds, 20.0) or n_img == 0:
+        oracle.sketched_pass_rei(x1_np[n_img % B], y_np[n_img % B], og, oidx, cfg.n_full, sigma,
+                                 args.seed, 0, n_img % B)
+        n_img += 1
+    cpu_s = time.perf_counter() - t0
+    line = {
+        "metric": f"REI sketched-EI operator passes/s at {cfg.N}², {cfg.n_full}→{m} angles",
+        "value": args.steps / (ms * 1e-3), "unit": "passes/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {**workload_desc(cfg, args.mode), "path": "skei_pass_rei (SURVEY 8(f) #3)",
+                   "rei_sigma": sigma, "launch": "one CUDA graph per step (draw + 6 launches)"},
+        "cpu_baseline": {"value": (n_img / B) / cpu_s, "unit": "passes/s", "cores": 1,
+                         "kind": "oracle", "sample": f"{n_img} image(s) through the oracle REI pass "
+                                                     f"({cpu_s:.1f} s; {B} images = 1 pass)"},
+        "gpu_launches": 7 * args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.path == "ei-grad":
         return run_ei_grad(args)
+    if args.path == "rei":
+        return run_rei(args)
     if args.split in ("angle", "angle-ag"):
         if args.config == "cfg3" and "--config" not in sys.argv:
             args.config = "cfg5"

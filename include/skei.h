@@ -258,6 +258,20 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const skei_pass_outputs *out, float *h_mc, float *h_ei,
                            void *ws, size_t ws_bytes, skei_stream stream);
 
+/* ---------------------------- next row: the REI variant of the pass --
+ * Robust EI: the EI branch reconstructs from simulated noisy measurements,
+ * x3 = F(A_S^+ (A_S x2 + sigma eps)).  Identical to skei_pass with x3 = NULL except
+ * q = ramp(p2 + sigma eps) (p2 is still reported noise-free; x_fbp, ei follow from q).
+ * eps[b][k][j] ~ N(0, 1): Box-Muller (cos branch) on words 2s, 2s+1 (s = k n_det + j) of
+ * the counter-based SplitMix64 stream keyed by (noise_seed, stream 5, noise_iter,
+ * image0 + b) — DESIGN.md R23; reproducible, independent of the launch configuration.
+ * sigma = 0 gives skei_pass's results.  Errors: as skei_pass; SKEI_ERR_ARG if sigma < 0. */
+skei_status skei_pass_rei(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                          const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                          int32_t idx_stride, float sigma, uint64_t noise_seed,
+                          uint64_t noise_iter, uint64_t image0, const skei_pass_outputs *out,
+                          void *ws, size_t ws_bytes, skei_stream stream);
+
 /* skei_pass with stage timing: `events` holds n_events (>= 6) cudaEvent_t handles
  * created by the caller, NULL entries skipped; event 0 is recorded before the first stage
  * and event i after stage i of: 1 rotate + packing, 2 forward (A_S x1 with the fused MC

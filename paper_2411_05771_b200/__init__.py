@@ -79,6 +79,8 @@ def lib():
             "skei_rotate_adjoint": ([vp, vp, vp, i32, vp, i32, vp], st),
             "skei_ei_grad": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, vp, sz, vp], st),
             "skei_fbp_adjoint": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
+            "skei_pass_rei": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, u64, u64,
+                               u64, vp, vp, sz, vp], st),
             "skei_backproject_band": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp,
                                        vp, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
@@ -365,6 +367,22 @@ def sketched_pass(plan: Plan, x1, y, g, idx, x3=None, out: dict | None = None,
                            _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
                            _ptr(x3, name="x3"), ctypes.byref(po), _ptr(ws, torch.uint8, "ws"),
                            ws.numel(), _stream(x1)), "skei_pass")
+    return out
+
+
+def sketched_pass_rei(plan: Plan, x1, y, g, idx, sigma: float, noise_seed: int, noise_iter: int,
+                      image0: int = 0, out: dict | None = None, ws: torch.Tensor | None = None):
+    """skei_pass_rei: the REI pass, q = ramp(p2 + sigma eps) (SURVEY 8(f) #3)."""
+    B, m = x1.shape[0], idx.shape[-1]
+    out = alloc_pass_outputs(plan, B, m, x1.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    po = _pass_out(out)
+    _check(lib().skei_pass_rei(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
+                               _ptr(g, torch.int32, "g"), 0 if g.numel() == 1 else 1,
+                               _ptr(idx, torch.int32, "idx"), m, _idx_stride(idx, B, m),
+                               float(sigma), int(noise_seed), int(noise_iter), int(image0),
+                               ctypes.byref(po), _ptr(ws, torch.uint8, "ws"), ws.numel(),
+                               _stream(x1)), "skei_pass_rei")
     return out
 
 

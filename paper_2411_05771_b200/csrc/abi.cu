@@ -450,10 +450,17 @@ skei_status skei_ei_residual(const skei_plan *plan, const float *p1, const float
 
 namespace {
 
+// REI: the FBP of the EI branch sees p2 + sigma eps (rei.cu)
+struct ReiNoise {
+    float sigma;
+    uint64_t seed, iter, image0;
+};
+
 skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const float *y,
                      const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
                      int32_t idx_stride, const float *x3_in, const skei_pass_outputs *o,
-                     void *ws, size_t ws_bytes, cudaEvent_t const *ev, cudaStream_t s) {
+                     void *ws, size_t ws_bytes, cudaEvent_t const *ev, cudaStream_t s,
+                     const ReiNoise *rei = nullptr) {
     skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
     if (st != SKEI_OK) return st;
     if (!x1 || !y || !g_deg || !o || !ws) return SKEI_ERR_ARG;
@@ -499,8 +506,16 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr));
     SKEI_CUDA(mark(2));
-    // a4: q = ramp(p2); the same launch also copies r into the interleaved layout
-    SKEI_CUDA(launch_ramp(plan, o->p2, o->q, B * m, s, qi, m, 4, o->r, ri));
+    // a4: q = ramp(p2); the same launch also copies r into the interleaved layout.  REI:
+    // q = ramp(p2 + sigma eps), the noisy copy in the workspace (p2 stays noise-free)
+    const float *pin = o->p2;
+    if (rei) {
+        float *pn = ws_f(ws, wl.q);
+        SKEI_CUDA(launch_rei_noise(o->p2, pn, B, m, plan->n_det, rei->sigma, rei->seed,
+                                   rei->iter, rei->image0, plan->num_sms, s));
+        pin = pn;
+    }
+    SKEI_CUDA(launch_ramp(plan, pin, o->q, B * m, s, qi, m, 4, o->r, ri));
     SKEI_CUDA(mark(3));
     // a5 + a8 (+ a7 EI part when x3 is the identity network's x_fbp): x_fbp = (pi/2m) A_S^T q
     // and grad = 2 A_S^T r in one launch, ei = ||x2 - x_fbp||^2 fused into its epilogue
@@ -523,6 +538,17 @@ skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const f
                       void *ws, size_t ws_bytes, skei_stream stream) {
     return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, x3_in, o, ws, ws_bytes,
                     nullptr, (cudaStream_t)stream);
+}
+
+skei_status skei_pass_rei(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                          const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
+                          int32_t idx_stride, float sigma, uint64_t noise_seed,
+                          uint64_t noise_iter, uint64_t image0, const skei_pass_outputs *out,
+                          void *ws, size_t ws_bytes, skei_stream stream) {
+    if (!(sigma >= 0.f)) return SKEI_ERR_ARG;
+    const ReiNoise rei{sigma, noise_seed, noise_iter, image0};
+    return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, nullptr, out, ws,
+                    ws_bytes, nullptr, (cudaStream_t)stream, &rei);
 }
 
 skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1,

@@ -129,6 +129,10 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
                              const AdjEi *ei = nullptr, int row0 = 0, int rows = -1);
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
+// REI: pn = p + sigma eps (rei.cu; R23)
+cudaError_t launch_rei_noise(const float *p, float *pn, int B, int m, int n_det, float sigma,
+                             uint64_t seed, uint64_t iter, uint64_t image0, int num_sms,
+                             cudaStream_t s);
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi = nullptr, int m = 0, int bb = 0,
                         const float *rs = nullptr, float *ri = nullptr, float rscale = 1.f);
