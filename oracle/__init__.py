@@ -52,6 +52,8 @@ def _load():
         lib.oracle_rotate.argtypes = [dp, dp, i32, i32]
         lib.oracle_rotate_adj.argtypes = [dp, dp, i32, i32]
         lib.oracle_rei_noise.argtypes = [u64, u64, u64, i32, i32, dp]
+        lib.oracle_sketch_deviation.argtypes = [i32, i32, i32, ip, i32, i32, dp, dp,
+                                                ctypes.POINTER(ctypes.c_double)]
         lib.oracle_pass_rei.argtypes = [dp, dp, i32, i32, i32, i32, ip, i32, ctypes.c_double,
                                         u64, u64, u64, dp, dp, dp, dp, dp, dp, dp,
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -227,4 +229,16 @@ def sketched_pass_rei(x1, y, g: int, idx, n_full: int, sigma: float, seed: int, 
                             ctypes.byref(mc), ctypes.byref(ei))
     out["mc"], out["ei"] = mc.value, ei.value
     return out
+
+
+def sketch_deviation(v0, idx, n_full: int, n_det: int, iters: int):
+    """(lambda, v): power-iteration estimate of ||A^T (S^T S - I) A||_2 (oracle.c
+    oracle_sketch_deviation) from the start image v0 [N, N]."""
+    v0, idx = _d(v0), _i(idx)
+    N = v0.shape[-1]
+    v = np.empty((N, N))
+    lam = ctypes.c_double(0)
+    _load().oracle_sketch_deviation(N, n_det, n_full, _ip(idx), len(idx), int(iters), _dp(v0),
+                                    _dp(v), ctypes.byref(lam))
+    return lam.value, v
 

@@ -422,3 +422,50 @@ void oracle_ei_grad(const double *x1, int N, int n_det, int n_full, int g, const
     free(md);
     free(p);
 }
+
+/* ----------------------- Theorem-1 deviation (§8(f) #4) --
+ * delta = ||A^T (S^T S - I) A||_2 for the sqrt(n_full/m)-scaled row-subsampling sketch S of
+ * the sketched angles idx, i.e. the spectral norm of the symmetric operator
+ *   D v = (n_full / m) A_S^T A_S v - A^T A v
+ * (A: all n_full angles; the quantity bounding the sketched-vs-full EI regulariser in the
+ * proof of Theorem 1), estimated by plain power iteration from v0 (normalised
+ * to ||v|| = 1 first): v <- D v / ||D v||, lambda = ||D v|| (of the last iterate). */
+void oracle_sketch_deviation(int N, int n_det, int n_full, const int *idx, int m, int iters,
+                             const double *v0, double *v_out, double *lambda)
+{
+    size_t nn = (size_t)N * N;
+    int *all = (int *)malloc(sizeof(int) * (size_t)n_full);
+    double *v = (double *)malloc(sizeof(double) * nn);
+    double *u = (double *)malloc(sizeof(double) * nn);
+    double *w = (double *)malloc(sizeof(double) * nn);
+    double *pf = (double *)malloc(sizeof(double) * (size_t)n_full * n_det);
+    double *ps = (double *)malloc(sizeof(double) * (size_t)m * n_det);
+    for (int i = 0; i < n_full; ++i) all[i] = i;
+    double s = 0.0;
+    for (size_t i = 0; i < nn; ++i) s += v0[i] * v0[i];
+    s = sqrt(s);
+    for (size_t i = 0; i < nn; ++i) v[i] = v0[i] / s;
+    double lam = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        oracle_fwd(v, pf, N, n_det, n_full, all, n_full);
+        oracle_adj(pf, u, N, n_det, n_full, all, n_full, 1.0);          /* A^T A v */
+        oracle_fwd(v, ps, N, n_det, n_full, idx, m);
+        oracle_adj(ps, w, N, n_det, n_full, idx, m, (double)n_full / m); /* (n_full/m) A_S^T A_S v */
+        double nrm = 0.0;
+        for (size_t i = 0; i < nn; ++i) {
+            w[i] -= u[i];
+            nrm += w[i] * w[i];
+        }
+        lam = sqrt(nrm);
+        if (lam == 0.0) break;
+        for (size_t i = 0; i < nn; ++i) v[i] = w[i] / lam;
+    }
+    if (v_out) memcpy(v_out, v, sizeof(double) * nn);
+    *lambda = lam;
+    free(all);
+    free(v);
+    free(u);
+    free(w);
+    free(pf);
+    free(ps);
+}

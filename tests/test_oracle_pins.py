@@ -559,3 +559,28 @@ def test_rei_monte_carlo_noise_inflation():
     d = np.array([np.sum((oracle.sketched_pass_rei(x1, y, g, idx, n_full, sigma, 0, it, 0)["xfbp"]
                           - plain) ** 2) for it in range(400)])
     assert abs(d.mean() - expect) <= 4 * d.std(ddof=1) / np.sqrt(len(d))
+
+
+# ------------------------------------------- Theorem-1 deviation
+def test_sketch_deviation_equals_dense_spectral_norm():
+    """Power iteration of D = (n_full/m) A_S^T A_S - A^T A (oracle) vs numpy's spectral norm
+    of the dense D built from the formula matrix (8x8, n_full = 8, m = 4)."""
+    N, n_det, n_full = 8, 12, 8
+    idx = np.array([1, 2, 5, 7])
+    A = _dense_A(N, n_det, n_full, np.arange(n_full))
+    AS = _dense_A(N, n_det, n_full, idx)
+    D = (n_full / len(idx)) * AS.T @ AS - A.T @ A
+    ref = np.linalg.norm(D, 2)
+    lam, v = oracle.sketch_deviation(np.random.default_rng(2).standard_normal((N, N)), idx,
+                                     n_full, n_det, 3000)
+    assert abs(lam - ref) <= 1e-6 * ref
+    # the iterate is an eigenvector of D for an eigenvalue of modulus ||D||
+    Dv = D @ v.ravel()
+    assert abs(np.linalg.norm(Dv) - ref) <= 1e-6 * ref
+
+
+def test_sketch_deviation_full_sketch_is_zero():
+    """m = n_full: S^T S = I, so the deviation vanishes exactly (SURVEY §8(c) sketch reduction)."""
+    N, n_det, n_full = 8, 12, 8
+    lam, _ = oracle.sketch_deviation(np.ones((N, N)), np.arange(n_full), n_full, n_det, 5)
+    assert lam < 1e-10
