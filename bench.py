@@ -54,7 +54,7 @@ def parse():
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
                          "BASELINE cfg5); angle-ag: the same split exchanging filtered "
                          "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2)")
-    ap.add_argument("--path", default="pass", choices=["pass", "ei-grad", "rei"],
+    ap.add_argument("--path", default="pass", choices=["pass", "ei-grad", "rei", "deviation"],
                     help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
                          "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad); "
                          "rei: the REI pass, q = ramp(p2 + sigma eps) (skei_pass_rei)")
@@ -412,8 +412,62 @@ def run_rei(args):
     return 0
 
 
+def run_deviation(args):
+    """--path deviation (one GPU): the Theorem-1 deviation
+    ||A^T (S^T S - I) A||_2 at the config's geometry for sketch sizes n_full/8 .. n_full/2
+    (interleaved sketches), `--steps` power iterations each from a random start image; the
+    timed unit is one power iteration (2 forward projections: all n_full angles and the
+    sketch, 2 backprojections, 1 norm), CUDA events, one stream."""
+    import torch
+
+    import paper_2411_05771_b200 as sk
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len, device=0)
+    v0 = torch.from_numpy(np.random.default_rng(args.seed).standard_normal(
+        (1, cfg.N, cfg.N)).astype(np.float32)).to(dev)
+    ws = plan.workspace(1, cfg.n_full)
+    table, ms_it = {}, None
+    mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    with ClockSampler(0) as clk:
+        for div in (8, 4, 2):
+            m = cfg.n_full // div
+            _, idx = sk.draw(args.seed, 0, sk.SHARED_IMAGE, cfg.n_full, m, sk.MODE_INTERLEAVED)
+            it = torch.tensor(idx, dtype=torch.int32, device=dev)
+            sk.sketch_deviation(plan, it, v0.clone(), args.warmup, ws=ws)
+            a, b = mk(), mk()
+            v = v0.clone()
+            a.record()
+            lam = sk.sketch_deviation(plan, it, v, args.steps, ws=ws)
+            b.record()
+            torch.cuda.synchronize()
+            table[str(m)] = float(lam[0])
+            if m == cfg.m:
+                ms_it = a.elapsed_time(b) / args.steps
+    line = {
+        "metric": f"Theorem-1 deviation power iterations/s at {cfg.N}², {cfg.n_full} angles, m={cfg.m}",
+        "value": 1e3 / ms_it if ms_it else None, "unit": "iterations/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_it,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"{cfg.name} geometry: {cfg.N}x{cfg.N}, "
+                                                    f"{cfg.n_full} angles, {cfg.n_det} bins, one "
+                                                    "random start image, interleaved sketches",
+                                        "l2": "not flushed (iterative: each iteration reads the "
+                                              "previous one's output)",
+                                        "launch": "direct, 8 launches per iteration",
+                                        "path": "skei_sketch_deviation (SURVEY 8(f) #4)"},
+        "delta_by_m": table, "gpu_launches": 8 * args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.path == "deviation":
+        return run_deviation(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.path == "ei-grad":

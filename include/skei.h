@@ -160,6 +160,20 @@ skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float 
                                   float *grad_band, float *ei_band, void *ws, size_t ws_bytes,
                                   skei_stream stream);
 
+/* ------------------- next row: the Theorem-1 sketching deviation --
+ * delta = ||A^T (S^T S - I) A||_2 (Theorem 1, proof L575-L583) for the
+ * sqrt(n_full/m)-scaled row subsampling onto the sketched angles idx, by `iters` power
+ * iterations on D v = (n_full/m) A_S^T A_S v - A^T A v (A: all n_full angles), batched
+ * over B independent start images.  v: [B][n][n] device, in: start vectors (normalised
+ * first), out: the last normalised iterate; lambda: [B] device, out: ||D v|| of the last
+ * iteration (-> delta).  The operators are the pass's kernels (packing, forward projector,
+ * backprojector accumulating into a base); the norms are fixed-order fp64 reductions.
+ * ws >= skei_workspace_bytes(plan, B, n_full) (NOTE: n_full, not m).
+ * Errors: SKEI_ERR_SHAPE (B, m), SKEI_ERR_ARG (NULL, iters < 1, strides, ws too small). */
+skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_t *idx,
+                                  int32_t m, int32_t idx_stride, int32_t iters, float *v,
+                                  float *lambda, void *ws, size_t ws_bytes, skei_stream stream);
+
 /* The transpose of skei_fbp (next row): p = (pi / 2 m_total) ramp(A_S x)
  * (the ramp kernel is even, so ramp is symmetric), i.e. the vector-Jacobian product of
  * the sketched FBP.  x: [B][n][n], p: [B][m][n_det] device; other arguments and errors as

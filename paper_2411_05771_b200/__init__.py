@@ -81,6 +81,7 @@ def lib():
             "skei_fbp_adjoint": ([vp, vp, vp, i32, vp, i32, i32, i32, vp, sz, vp], st),
             "skei_pass_rei": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, u64, u64,
                                u64, vp, vp, sz, vp], st),
+            "skei_sketch_deviation": ([vp, i32, vp, i32, i32, i32, vp, vp, vp, sz, vp], st),
             "skei_backproject_band": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp,
                                        vp, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
@@ -262,6 +263,20 @@ def backproject_band(plan: Plan, q: torch.Tensor, r: torch.Tensor, idx: torch.Te
                                        _ptr(ei, name="ei"), _ptr(ws, torch.uint8, "ws"),
                                        ws.numel(), _stream(q)), "skei_backproject_band")
     return xf, gr, ei
+
+
+def sketch_deviation(plan: Plan, idx: torch.Tensor, v: torch.Tensor, iters: int,
+                     ws: torch.Tensor | None = None):
+    """skei_sketch_deviation: ||A^T (S^T S - I) A||_2 by power iteration from the start images
+    v [B][n][n] (overwritten by the last iterate).  Returns lambda [B]."""
+    B, m = v.shape[0], idx.shape[-1]
+    lam = torch.empty(B, dtype=torch.float32, device=v.device)
+    ws = plan.workspace(B, plan.n_full) if ws is None else ws
+    _check(lib().skei_sketch_deviation(plan.handle, B, _ptr(idx, torch.int32, "idx"), m,
+                                       _idx_stride(idx, B, m), int(iters), _ptr(v, name="v"),
+                                       _ptr(lam, name="lambda"), _ptr(ws, torch.uint8, "ws"),
+                                       ws.numel(), _stream(v)), "skei_sketch_deviation")
+    return lam
 
 
 def ei_grad(plan: Plan, x2: torch.Tensor, x3: torch.Tensor, g: torch.Tensor, idx: torch.Tensor,

@@ -54,7 +54,7 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // Workspace: [q: B*m*n_det floats][residual partials][4 packed images: x1 rows/cols, x2
 // rows/cols, each pack_floats() for the largest image group]
 struct WsLayout {
-    size_t q, res, pack[4], ctr, mcpart, eipart, fscr, qi, ri, total;
+    size_t q, res, pack[4], ctr, mcpart, eipart, fscr, qi, ri, aux, total;
 };
 WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     WsLayout w;
@@ -84,6 +84,8 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     off += align256(sizeof(float) * adj_il_floats(plan, B, m));
     w.ri = off;
     off += align256(sizeof(float) * adj_il_floats(plan, B, m));
+    w.aux = off;  // skei_sketch_deviation: the full angle list and per-image fp64 norms
+    off += align256(sizeof(int32_t) * (size_t)plan->n_full) + align256(sizeof(double) * (size_t)B);
     w.total = off;
     return w;
 }
@@ -401,6 +403,46 @@ skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float 
     AdjJob aj[2] = {{q, xfbp_band, (float)(M_PI / (2.0 * (double)m_total))}, {r, grad_band, 2.0f}};
     AdjEi eif{x2, ws_f(ws, wl.eipart), ctr + 1, ei_band};
     SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, &eif, row0, rows));
+    return SKEI_OK;
+}
+
+skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_t *idx,
+                                  int32_t m, int32_t idx_stride, int32_t iters, float *v,
+                                  float *lambda, void *ws, size_t ws_bytes, skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!v || !lambda || !ws || iters < 1) return SKEI_ERR_ARG;
+    const int nf = plan->n_full;
+    if (ws_bytes < skei_workspace_bytes(plan, B, nf)) return SKEI_ERR_ARG;
+    DeviceGuard guard(plan->device);
+    const WsLayout w = ws_layout(plan, B, nf);  // sized for the full angle set
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
+    int32_t *all = reinterpret_cast<int32_t *>(ws_f(ws, w.aux));
+    double *norm2 = reinterpret_cast<double *>((char *)ws + w.aux +
+                                               align256(sizeof(int32_t) * (size_t)nf));
+    float *pf = ws_f(ws, w.q), *ps = ws_f(ws, w.ri);
+    float *u = ws_f(ws, w.pack[2]), *dv = ws_f(ws, w.pack[3]);
+    const long per = (long)plan->n * plan->n;
+    SKEI_CUDA(launch_iota(all, nf, s));
+    // v <- v / ||v||
+    SKEI_CUDA(launch_sumsq(v, B, per, norm2, s));
+    SKEI_CUDA(launch_normalise(v, v, B, per, norm2, nullptr, plan->num_sms, s));
+    const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
+    for (int it = 0; it < iters; ++it) {
+        RotPackJob pj{v, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+        SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, 0), s));
+        FwdJob ff{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), pf, nullptr, nullptr};
+        SKEI_CUDA(launch_radon_fwd(plan, &ff, 1, B, all, nf, 0, scr, s));   // A v
+        FwdJob fs{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ps, nullptr, nullptr};
+        SKEI_CUDA(launch_radon_fwd(plan, &fs, 1, B, idx, m, idx_stride, scr, s));  // A_S v
+        AdjJob a1{pf, u, -1.0f};  // u = -A^T A v
+        SKEI_CUDA(launch_radon_adj(plan, &a1, 1, B, all, nf, 0, s));
+        AdjJob a2{ps, dv, (float)((double)nf / m), nullptr, u};  // D v = u + (n_full/m) A_S^T A_S v
+        SKEI_CUDA(launch_radon_adj(plan, &a2, 1, B, idx, m, idx_stride, s));
+        SKEI_CUDA(launch_sumsq(dv, B, per, norm2, s));
+        SKEI_CUDA(launch_normalise(dv, v, B, per, norm2, lambda, plan->num_sms, s));
+    }
     return SKEI_OK;
 }
 
