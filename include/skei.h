@@ -59,7 +59,7 @@ typedef void *skei_stream; /* cudaStream_t */
 /* Geometry of one CT system: n x n images, n_det detector bins, n_full angles on
  * [0, pi).  fft_len = ramp FFT length P: a power of two >= 2*n_det - 1 (the length
  * at which the zero-padded circular convolution equals the linear one, DESIGN.md
- * §7 "k_ramp"); 0 selects the smallest such power of two.  Limits: 2 <= n <= 1792
+ * §7 "k_ramp"); 0 selects the smallest such power of two.  Limits: 2 <= n <= 1536
  * (a line block of the forward projector, (n + 8) x 128 bytes, must fit in one SM's
  * shared memory), 1 <= n_det <= 3072, 1 <= n_full <= 16384, 16 <= P <= 8192 (fft_len 0
  * selects max(16, pow2 >= 2 n_det - 1)). */

@@ -123,7 +123,7 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     if (!geom || !out) return SKEI_ERR_ARG;
     *out = nullptr;
     const int n = geom->n, n_det = geom->n_det, n_full = geom->n_full;
-    if (n < 2 || n > 1792 || n_det < 1 || n_det > 3072 || n_full < 1 || n_full > 16384)
+    if (n < 2 || n > 1536 || n_det < 1 || n_det > 3072 || n_full < 1 || n_full > 16384)
         return SKEI_ERR_CONFIG;
     int P = geom->fft_len;
     if (P == 0) {

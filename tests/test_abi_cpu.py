@@ -50,6 +50,8 @@ def test_host_validation_without_device():
     assert L.skei_plan_create(ctypes.byref(g), 0, ctypes.byref(h)) == 2
     g = sk._Geom(64, 91, 32, 128)  # 128 < 2*91-1 -> config error
     assert L.skei_plan_create(ctypes.byref(g), 0, ctypes.byref(h)) == 2
+    g = sk._Geom(1537, 2174, 32, 0)  # n > 1536: a line block would not fit shared memory
+    assert L.skei_plan_create(ctypes.byref(g), 0, ctypes.byref(h)) == 2
     if not torch.cuda.is_available():
         g = sk._Geom(64, 91, 32, 0)
         assert L.skei_plan_create(ctypes.byref(g), 0, ctypes.byref(h)) == 5  # no device

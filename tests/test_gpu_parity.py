@@ -212,6 +212,26 @@ def test_pass_parity_full_size(name):
     _check_pass(cfg, sorted({0, cfg.B - 1}))
 
 
+@pytest.mark.parametrize("N,n_det,n_full,P,B,m", [
+    (1536, 2173, 32, 8192, 1, 4),   # the largest image the ABI accepts (n <= 1536), P = 8192
+    (256, 3072, 16, 8192, 4, 4),    # the widest detector (n_det <= 3072): one angle per unit
+])
+def test_pass_parity_max_geometry(N, n_det, n_full, P, B, m):
+    """The ABI's size limits (include/skei.h): every output of the pass against the oracle."""
+    plan = sk.Plan.get(N, n_det, n_full, P)
+    rng = np.random.default_rng(N)
+    x1 = synth.rand_images(B, N, 21)
+    y = rng.standard_normal((B, n_full, n_det)).astype(np.float32)
+    g, idx = sk.draw(5, 1, SH, n_full, m)
+    out = sk.sketched_pass(plan, dev(x1), dev(y), idx_t([g]), idx_t(idx))
+    for b in range(B):
+        ref = oracle.sketched_pass(x1[b], y[b], g, idx, n_full)
+        for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad"):
+            close(out[k][b], ref[k], f"max geom {k} b={b}")
+        for k in ("mc", "ei"):
+            assert abs(float(out[k][b]) - ref[k]) <= TOL * abs(ref[k]), k
+
+
 def test_pass_deterministic_bitwise():
     cfg = synth.CONFIGS["cfg2"]
     plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
