@@ -48,12 +48,14 @@ def parse():
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
     ap.add_argument("--mode", default="uniform", choices=["uniform", "interleaved"])
-    ap.add_argument("--split", default="batch", choices=["batch", "angle", "angle-ag"],
+    ap.add_argument("--split", default="batch", choices=["batch", "angle", "angle-ag", "angle-p2p"],
                     help="batch: every rank runs its own batch (weak scaling, no collective); "
                          "angle: one batch, the sketch's angles split over the ranks with one "
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
                          "BASELINE cfg5); angle-ag: the same split exchanging filtered "
-                         "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2)")
+                         "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2); "
+                         "angle-p2p: the same with the exchange fused into the ramp kernel "
+                         "(P2P stores into symmetric memory, no NCCL on the data path)")
     ap.add_argument("--path", default="pass", choices=["pass", "ei-grad", "rei", "deviation"],
                     help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
                          "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad); "
@@ -215,7 +217,8 @@ def run_angle(args):
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    split_fn = skdist.angle_split_pass_allgather if args.split == "angle-ag" else skdist.angle_split_pass
+    split_fn = {"angle-ag": skdist.angle_split_pass_allgather,
+                "angle-p2p": skdist.angle_split_pass_p2p}.get(args.split, skdist.angle_split_pass)
 
     def step(it):
         g, idx = sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, cfg.m, mode)
@@ -250,10 +253,12 @@ def run_angle(args):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {**workload_desc(cfg, args.mode),
-                       "parallelism": f"angle split x{world}" + (" (all-gather of filtered rows, "
-                                                                   "row-band backprojection)"
-                                                                   if args.split == "angle-ag" else ""),
+                       "parallelism": f"angle split x{world}" + {
+                           "angle-ag": " (NCCL all-gather of filtered rows, row-band backprojection)",
+                           "angle-p2p": " (filtered rows stored to every rank by the ramp kernel "
+                                        "over NVLink P2P, row-band backprojection)"}.get(args.split, ""),
                        **({"allgather_bytes": int(out["allgather_bytes"])} if args.split == "angle-ag"
+                          else {"p2p_bytes": int(out["p2p_bytes"])} if args.split == "angle-p2p"
                           else {"allreduce_bytes": int(out["allreduce_bytes"])}),
                        "launch": "direct (not graphed): library calls + NCCL collectives"},
             "clocks": clk.summary(),
@@ -474,7 +479,7 @@ def main():
         return run_ei_grad(args)
     if args.path == "rei":
         return run_rei(args)
-    if args.split in ("angle", "angle-ag"):
+    if args.split in ("angle", "angle-ag", "angle-p2p"):
         if args.config == "cfg3" and "--config" not in sys.argv:
             args.config = "cfg5"
         return run_angle(args)

@@ -153,6 +153,20 @@ skei_status skei_rotate_adjoint(const skei_plan *plan, const float *y, float *ou
  * (whole images); xfbp_band, grad_band: [B][rows][n]; ei_band: [B]; all device.
  * Errors: SKEI_ERR_SHAPE (B, m, or the band outside [0, n)), SKEI_ERR_ARG (NULL, strides,
  * m_total < m, ws too small). */
+/* The fused exchange of that split (no NCCL on the data path): q = ramp(p) for this
+ * rank's m_local sketched rows (written to q_local [B][m_local][n_det]) with every output
+ * row ALSO stored, from the ramp kernel's last pass, into row (b, row0 + k) of each of the
+ * n_peers buffers peer_q[g] [B][m_total][n_det] — device pointers valid on this GPU
+ * (NVLink P2P / symmetric memory, this rank's own buffer among them) — and the residual
+ * rows r [B][m_local][n_det] likewise into peer_r[g].  The transfer overlaps the FFT tile
+ * by tile; after a cross-rank barrier every rank holds the whole q and r for
+ * skei_backproject_band.  peer_q, peer_r: HOST arrays of n_peers (<= 8) device pointers.
+ * Errors: SKEI_ERR_SHAPE (B, m_local < 1, rows outside [0, m_total)), SKEI_ERR_ARG. */
+skei_status skei_ramp_allgather(const skei_plan *plan, int32_t B, const float *p,
+                                const float *r, int32_t m_local, int32_t row0, int32_t m_total,
+                                float *q_local, float *const *peer_q, float *const *peer_r,
+                                int32_t n_peers, skei_stream stream);
+
 skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float *q,
                                   const float *r, const int32_t *idx, int32_t m,
                                   int32_t idx_stride, int32_t m_total, const float *x2,

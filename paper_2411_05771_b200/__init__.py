@@ -82,6 +82,7 @@ def lib():
             "skei_pass_rei": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, u64, u64,
                                u64, vp, vp, sz, vp], st),
             "skei_sketch_deviation": ([vp, i32, vp, i32, i32, i32, vp, vp, vp, sz, vp], st),
+            "skei_ramp_allgather": ([vp, i32, vp, vp, i32, i32, i32, vp, vp, vp, i32, vp], st),
             "skei_backproject_band": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp,
                                        vp, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
@@ -244,6 +245,21 @@ def fbp_adjoint(plan: Plan, x: torch.Tensor, idx: torch.Tensor, m_total: int | N
                                   int(m_total or m), _ptr(ws, torch.uint8, "ws"), ws.numel(),
                                   _stream(x)), "skei_fbp_adjoint")
     return p
+
+
+def ramp_allgather(plan: Plan, p: torch.Tensor, r: torch.Tensor, row0: int, m_total: int,
+                   peer_q: list, peer_r: list, q_local: torch.Tensor | None = None):
+    """skei_ramp_allgather: q_local = ramp(p) and, fused in the same kernel, every row of q and
+    of r stored into rows row0.. of each peer buffer (device pointers, ints)."""
+    B, m_local = p.shape[0], p.shape[1]
+    q_local = torch.empty_like(p) if q_local is None else q_local
+    n = len(peer_q)
+    arr_q = (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(x)) for x in peer_q])
+    arr_r = (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(x)) for x in peer_r])
+    _check(lib().skei_ramp_allgather(plan.handle, B, _ptr(p, name="p"), _ptr(r, name="r"), m_local,
+                                     int(row0), int(m_total), _ptr(q_local, name="q_local"), arr_q,
+                                     arr_r, n, _stream(p)), "skei_ramp_allgather")
+    return q_local
 
 
 def backproject_band(plan: Plan, q: torch.Tensor, r: torch.Tensor, idx: torch.Tensor,

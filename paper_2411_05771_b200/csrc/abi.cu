@@ -446,6 +446,29 @@ skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_
     return SKEI_OK;
 }
 
+skei_status skei_ramp_allgather(const skei_plan *plan, int32_t B, const float *p,
+                                const float *r, int32_t m_local, int32_t row0, int32_t m_total,
+                                float *q_local, float *const *peer_q, float *const *peer_r,
+                                int32_t n_peers, skei_stream stream) {
+    if (!plan || !p || !r || !q_local || !peer_q || !peer_r) return SKEI_ERR_ARG;
+    if (B < 1 || m_local < 1 || row0 < 0 || row0 + m_local > m_total) return SKEI_ERR_SHAPE;
+    if (n_peers < 1 || n_peers > kMaxPeers) return SKEI_ERR_ARG;
+    RampPeers pr;
+    pr.n = n_peers;
+    for (int g = 0; g < kMaxPeers; ++g) {
+        pr.q[g] = g < n_peers ? peer_q[g] : nullptr;
+        pr.r[g] = g < n_peers ? peer_r[g] : nullptr;
+        if (g < n_peers && (!pr.q[g] || !pr.r[g])) return SKEI_ERR_ARG;
+    }
+    pr.m_local = m_local;
+    pr.row0 = row0;
+    pr.m_total = m_total;
+    DeviceGuard guard(plan->device);
+    SKEI_CUDA(launch_ramp(plan, p, q_local, B * m_local, (cudaStream_t)stream, nullptr, 0, 0, r,
+                          nullptr, 1.f, &pr));
+    return SKEI_OK;
+}
+
 skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, int32_t B,
                              const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
                              void *ws, size_t ws_bytes, skei_stream stream) {

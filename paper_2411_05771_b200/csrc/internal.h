@@ -138,9 +138,19 @@ cudaError_t launch_iota(int32_t *a, int n, cudaStream_t s);
 cudaError_t launch_rei_noise(const float *p, float *pn, int B, int m, int n_det, float sigma,
                              uint64_t seed, uint64_t iter, uint64_t image0, int num_sms,
                              cudaStream_t s);
+// peers of the fused all-gather (ramp.cu): local rows (b, k) of q and r also go to rows
+// (b, row0 + k) of every peer's [B][m_total][n_det] q and r buffers
+constexpr int kMaxPeers = 8;
+struct RampPeers {
+    int n;
+    float *q[kMaxPeers];
+    float *r[kMaxPeers];
+    int m_local, row0, m_total;
+};
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi = nullptr, int m = 0, int bb = 0,
-                        const float *rs = nullptr, float *ri = nullptr, float rscale = 1.f);
+                        const float *rs = nullptr, float *ri = nullptr, float rscale = 1.f,
+                        const RampPeers *peers = nullptr);
 
 // Residual: partials in ws (float2 per (image, chunk)), then final reduce.
 size_t residual_ws_bytes(const skei_plan *plan, int B, int m);

@@ -99,6 +99,13 @@ struct RampArgs {
     const float *rs;
     float *ri;
     int nramp;
+    // optional peer outputs (the fused all-gather of the single-image angle split, SURVEY
+    // §8(f) #2): local row (b, k) of q — and, by CTAs nramp.., of rs — is also stored into
+    // row (b, row0 + k) of every peer's [B][m_total][n_det] buffer (P2P stores over
+    // NVLink; one of the peers is this GPU's own buffer)
+    float *pq[kMaxPeers];
+    float *pr[kMaxPeers];
+    int npeer, m_local, row0, m_total;
 };
 __device__ __forceinline__ float *il_row(const RampArgs &a, int row) {
     const int b = row / a.m, k = row - b * a.m;
@@ -110,9 +117,10 @@ __device__ __forceinline__ float *il_row(const RampArgs &a, int row) {
 // R[i] as loaded (first inverse pass), kOut = write the two output rows to global (last
 // inverse pass); otherwise smem -> smem.
 constexpr int kIn = 1, kScale = 2, kOut = 4;
-template <int R>
+template <int R, bool PEERS>
 __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool inverse, int mode,
-                                     const float *pa, const float *pb, float *qa, float *qb, float *ia, float *ib) {
+                                     const float *pa, const float *pb, float *qa, float *qb, float *ia, float *ib,
+                                     long peer_a, long peer_b) {
     constexpr int J = 16 / R;
     // every pass before `ip` is radix 16: Ns = 16^ip, table offset = sum_{i<ip} 16 * 16^i
     const int Ns = 1 << (4 * ip), stride = a.P / R;
@@ -161,6 +169,13 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
                         ia[(long)o * a.bb] = v[jj][q].x;
                         if (ib) ib[(long)o * a.bb] = v[jj][q].y;
                     }
+                    if constexpr (PEERS) {
+#pragma unroll 1
+                        for (int g = 0; g < a.npeer; ++g) {
+                            a.pq[g][peer_a + o] = v[jj][q].x;
+                            if (qb) a.pq[g][peer_b + o] = v[jj][q].y;
+                        }
+                    }
                 }
             }
         } else {
@@ -172,9 +187,25 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
 }
 
 // MAXT: P/16 <= MAXT threads; MINB: resident CTAs per SM the register budget must allow
-template <int RL, int MAXT, int MINB>
+template <int RL, int MAXT, int MINB, bool PEERS>
 __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
     extern __shared__ float2 z[];
+    // global row of local row `row` in the peers' [B][m_total][n_det] buffers
+    auto peer_off = [&](int row) -> long {
+        const int b = row / a.m_local, k = row - b * a.m_local;
+        return ((long)b * a.m_total + a.row0 + k) * a.n_det;
+    };
+    if (PEERS && (int)blockIdx.x >= a.nramp) {  // copy local r row u to every peer
+        const int u = blockIdx.x - a.nramp;
+        const float *src = a.rs + (long)u * a.n_det;
+        const long off = peer_off(u);
+        for (int j = threadIdx.x; j < a.n_det; j += blockDim.x) {
+            const float v = __ldg(src + j);
+#pragma unroll 1
+            for (int g = 0; g < a.npeer; ++g) a.pr[g][off + j] = v;
+        }
+        return;
+    }
     if ((int)blockIdx.x >= a.nramp) {  // interleave r: group g = u / m of 4 images, angle k
         const int u = blockIdx.x - a.nramp, g = u / a.m, k = u - g * a.m;
         const long stride = (long)a.m * a.n_det;  // between images
@@ -198,15 +229,17 @@ __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
     float *qb = has_b ? a.q + (long)rb * a.n_det : nullptr;
     float *ia = a.qi ? il_row(a, ra) : nullptr;
     float *ib = a.qi && has_b ? il_row(a, rb) : nullptr;
+    const long pa_off = PEERS ? peer_off(ra) : 0, pb_off = PEERS && has_b ? peer_off(rb) : 0;
     const int last = a.npass - 1;
     // forward: radix-16 passes then the RL pass
     for (int ip = 0; ip < last; ++ip)
-        pass<16>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib);
-    pass<RL>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib);
+        pass<16, PEERS>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
+    pass<RL, PEERS>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
     // inverse of R . FFT(z)
     for (int ip = 0; ip < last; ++ip)
-        pass<16>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb, ia, ib);
-    pass<RL>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb, ia, ib);
+        pass<16, PEERS>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
+    pass<RL, PEERS>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb, ia, ib,
+                    pa_off, pb_off);
     if (ia) {  // the zero pads of the interleaved rows
         for (int t = threadIdx.x; t < 2 * kAdjPad; t += blockDim.x) {
             const int o = t < kAdjPad ? t - kAdjPad : a.n_det + (t - kAdjPad);
@@ -245,8 +278,16 @@ void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal) 
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi, int m, int bb, const float *rs, float *ri,
-                        float rscale) {
+                        float rscale, const RampPeers *peers) {
     RampArgs a;
+    a.npeer = peers ? peers->n : 0;
+    for (int g = 0; g < kMaxPeers; ++g) {
+        a.pq[g] = peers && g < peers->n ? peers->q[g] : nullptr;
+        a.pr[g] = peers && g < peers->n ? peers->r[g] : nullptr;
+    }
+    a.m_local = peers ? peers->m_local : 1;
+    a.row0 = peers ? peers->row0 : 0;
+    a.m_total = peers ? peers->m_total : 1;
     a.rs = rs;
     a.ri = ri;
     a.qi = qi;
@@ -266,15 +307,24 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     const size_t smem = sizeof(float2) * (size_t)(a.P + a.P / 16);
     const int threads = a.P / 16;
     a.nramp = (rows + 1) / 2;
-    // + the interleaving CTAs of r (rows / m images in groups of 4, m angles each)
-    const int grid = a.nramp + (ri && rs ? (rows / a.m / 4) * a.m : 0);
+    // + the interleaving CTAs of r (rows / m images in groups of 4, m angles each), or with
+    // peers the CTAs that copy each local r row to the peers
+    const bool pe = peers && peers->n > 0;
+    const int grid = a.nramp + (pe ? (rs ? rows : 0) : (ri && rs ? (rows / a.m / 4) * a.m : 0));
     cudaError_t e = cudaSuccess;
-#define SKEI_RAMP_LAUNCH3(RLV, MT, MB)                                                          \
+#define SKEI_RAMP_LAUNCH4(RLV, MT, MB, PE)                                                      \
     do {                                                                                        \
         if (smem > 48 * 1024)                                                                   \
-            e = cudaFuncSetAttribute(k_ramp<RLV, MT, MB>,                                       \
+            e = cudaFuncSetAttribute(k_ramp<RLV, MT, MB, PE>,                                   \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
-        if (e == cudaSuccess) k_ramp<RLV, MT, MB><<<grid, threads, smem, s>>>(a);              \
+        if (e == cudaSuccess) k_ramp<RLV, MT, MB, PE><<<grid, threads, smem, s>>>(a);          \
+    } while (0)
+#define SKEI_RAMP_LAUNCH3(RLV, MT, MB)                  \
+    do {                                                \
+        if (pe)                                         \
+            SKEI_RAMP_LAUNCH4(RLV, MT, MB, true);       \
+        else                                            \
+            SKEI_RAMP_LAUNCH4(RLV, MT, MB, false);      \
     } while (0)
     // small transforms (P <= 2048, <= 128 threads): <= 64 registers so 8 CTAs fit an SM
 #define SKEI_RAMP_LAUNCH(RLV)                      \
@@ -292,6 +342,7 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     }
 #undef SKEI_RAMP_LAUNCH
 #undef SKEI_RAMP_LAUNCH3
+#undef SKEI_RAMP_LAUNCH4
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -32,7 +32,8 @@ import torch
 import torch.distributed as dist
 
 __all__ = ["batch_range", "angle_shard", "CudaOps", "angle_split_pass", "batch_split_images",
-           "angle_split_pass_allgather", "shard_phase", "band_phase"]
+           "angle_split_pass_allgather", "shard_phase", "band_phase", "angle_split_pass_p2p",
+           "P2PBuffers", "simulate_p2p_split"]
 
 
 def batch_range(B: int, rank: int, world: int) -> range:
@@ -97,6 +98,10 @@ class CudaOps:
     def backproject_band(self, q, r, idx, x2, row0, rows, m_total):
         import paper_2411_05771_b200 as sk
         return sk.backproject_band(self.plan, q, r, idx, x2, row0, rows, m_total=m_total)
+
+    def ramp_allgather(self, p, r, row0, m_total, peer_q, peer_r):
+        import paper_2411_05771_b200 as sk
+        return sk.ramp_allgather(self.plan, p, r, row0, m_total, peer_q, peer_r)
 
 
 def angle_split_pass(ops, x1, y, g, idx, group=None):
@@ -206,4 +211,92 @@ def angle_split_pass_allgather(ops, x1, y, g, idx, group=None):
 def allgather_bytes(B: int, m: int, n_det: int) -> int:
     """Bytes all ranks contribute to the exchange of the all-gather split: 2 B m n_det fp32."""
     return 4 * 2 * B * m * n_det
+
+
+# ---------------------------------------------------------------------------------------
+# The same split with the exchange fused into the ramp kernel (SURVEY §8(f) #2, no NCCL on
+# the data path): every rank's ramp kernel stores each filtered row — and each residual row —
+# straight into the full-size q and r buffers of EVERY rank (P2P stores over NVLink into
+# symmetric memory, its own buffer among them), so the 2.97 MB all-gather overlaps the FFT
+# tile by tile; a device-side barrier then releases the row-band backprojection.
+
+class P2PBuffers:
+    """Full-size q and r buffers [B][m][n_det] on every rank plus the peers' pointers: torch
+    symmetric memory over the group (world > 1), or plain local tensors (world 1)."""
+
+    def __init__(self, B, m, n_det, device, group=None):
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.world = world
+        if world > 1:
+            import torch.distributed._symmetric_memory as symm
+            grp = group if group is not None else dist.group.WORLD
+            if hasattr(symm, "enable_symm_mem_for_group"):
+                symm.enable_symm_mem_for_group(grp.group_name)
+            self.buf = symm.empty((2, B, m, n_det), dtype=torch.float32, device=device)
+            self.handle = symm.rendezvous(self.buf, grp.group_name)
+            step = B * m * n_det * 4
+            ptrs = [int(p) for p in self.handle.buffer_ptrs]
+            self.peer_q = ptrs
+            self.peer_r = [p + step for p in ptrs]
+        else:
+            self.buf = torch.empty((2, B, m, n_det), dtype=torch.float32, device=device)
+            self.handle = None
+            self.peer_q = [self.buf[0].data_ptr()]
+            self.peer_r = [self.buf[1].data_ptr()]
+        self.q, self.r = self.buf[0], self.buf[1]
+
+    def barrier(self):
+        """Every rank's stores have landed in every buffer (stream-ordered device barrier)."""
+        if self.handle is not None:
+            self.handle.barrier(channel=0)
+
+
+def angle_split_pass_p2p(ops, x1, y, g, idx, group=None, bufs: P2PBuffers | None = None):
+    """One pass with the sketch `idx` split over the ranks of `group`, the filtered and residual
+    rows exchanged by the ramp kernel's own P2P stores (module comment above); outputs as
+    angle_split_pass_allgather (row bands of x_fbp and grad, complete mc and ei)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    m = len(idx)
+    sub = angle_shard(idx, rank, world)
+    row0 = batch_range(m, rank, world).start
+    x2 = ops.rotate(x1, g)
+    p1 = ops.forward(x1, sub)
+    p2 = ops.forward(x2, sub)
+    mc_part, r = ops.residual(p1, y, sub)
+    B, n_det = p2.shape[0], p2.shape[-1]
+    if bufs is None:
+        bufs = P2PBuffers(B, m, n_det, p2.device, group)
+    ops.ramp_allgather(p2, r, row0, m, bufs.peer_q, bufs.peer_r)
+    bufs.barrier()
+    bd = band_phase(ops, bufs.q, bufs.r, idx, x2, rank, world)
+    scal = torch.cat([mc_part.to(bd["ei"].dtype), bd["ei"]])
+    if world > 1:
+        dist.all_reduce(scal, op=dist.ReduceOp.SUM, group=group)
+    return {"x2": x2, "xfbp": bd["xfbp"], "grad": bd["grad"], "rows": bd["rows"],
+            "mc": scal[:B], "ei": scal[B:], "idx": sub,
+            "p2p_bytes": 2 * B * len(sub) * n_det * 4 * world}
+
+
+def simulate_p2p_split(ops, x1, y, g, idx, world: int):
+    """The P2P split's data path on ONE GPU: `world` virtual ranks, each with its own full-size
+    q/r buffers; every virtual rank's ramp kernel stores its rows into all of them (the same
+    kernel and pointer lists as across GPUs), then each virtual rank backprojects its band.
+    Returns the per-rank band outputs and the shard scalars (test helper)."""
+    m = len(idx)
+    x2 = ops.rotate(x1, g)
+    B, n_det = x1.shape[0], ops.plan.n_det
+    bufs = [torch.empty((2, B, m, n_det), dtype=torch.float32, device=x1.device) for _ in range(world)]
+    peer_q = [b[0].data_ptr() for b in bufs]
+    peer_r = [b[1].data_ptr() for b in bufs]
+    mc = torch.zeros(B, dtype=torch.float32, device=x1.device)
+    for rk in range(world):
+        sub = angle_shard(idx, rk, world)
+        p1 = ops.forward(x1, sub)
+        p2 = ops.forward(x2, sub)
+        mc_part, r = ops.residual(p1, y, sub)
+        ops.ramp_allgather(p2, r, batch_range(m, rk, world).start, m, peer_q, peer_r)
+        mc += mc_part
+    bands = [band_phase(ops, bufs[rk][0], bufs[rk][1], idx, x2, rk, world) for rk in range(world)]
+    return {"x2": x2, "bands": bands, "mc": mc, "bufs": bufs}
 

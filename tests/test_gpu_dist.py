@@ -116,3 +116,41 @@ def test_allgather_split_single_rank_equals_pass():
     full = sk.sketched_pass(plan, x1, y, g, idx)
     for k in ("x2", "xfbp", "grad", "mc", "ei"):
         _close(out[k], full[k], k)
+
+
+@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 3), ("cfg5", 4), ("cfg5", 8)])
+def test_p2p_fused_allgather_split_tiles_full_pass(name, world):
+    """SURVEY §8(f) #2 with the exchange fused into the ramp kernel (P2P stores into every
+    rank's buffers), simulated on one GPU with `world` virtual ranks and real pointer lists:
+    every rank's buffers end up holding the whole q and r (identical to one ramp of the
+    full sketch), and the row bands tile x_fbp and grad of the single-GPU pass."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    out = skdist.simulate_p2p_split(skdist.CudaOps(plan), x1, y, g, idx[0], world)
+    for b in out["bufs"]:
+        _close(b[0], full["q"], "q in every rank's buffer")
+        _close(b[1], full["r"], "r in every rank's buffer")
+        assert torch.equal(b[0], out["bufs"][0][0]) and torch.equal(b[1], out["bufs"][0][1])
+    bands = out["bands"]
+    _close(torch.cat([bd["xfbp"] for bd in bands], dim=1), full["xfbp"], "xfbp bands")
+    _close(torch.cat([bd["grad"] for bd in bands], dim=1), full["grad"], "grad bands")
+    _close(out["mc"], full["mc"], "mc")
+    _close(sum(bd["ei"] for bd in bands), full["ei"], "ei")
+
+
+def test_p2p_split_single_rank_equals_pass():
+    cfg = synth.CONFIGS["cfg1"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    out = skdist.angle_split_pass_p2p(skdist.CudaOps(plan), x1, y, g, idx[0])
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    for k in ("x2", "xfbp", "grad", "mc", "ei"):
+        _close(out[k], full[k], k)
