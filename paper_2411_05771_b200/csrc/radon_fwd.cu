@@ -28,16 +28,18 @@
 //     banks, whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way
 //     conflicts at every angle with |beta| < 1 because 8 bins span more than 8 pixels), and
 //     consecutive lines differ in one bit, so the position moves by one add per line.
-//   * 640 threads (96 registers each), one CTA per SM.  Task = (angle, 32 consecutive
-//     bins), lane = bin; the K x chunks tasks are dealt round-robin to the 20 warps (each
-//     warp gets a mix of angles, whose footprints differ); a thread owns up to kMaxT tasks
-//     and keeps BB accumulators per task in registers: K = 20 kMaxT / chunks angles.
+//   * 512 threads (128 registers each), one CTA per SM.  Task = (angle, 32 consecutive
+//     bins), lane = bin; a thread owns up to kMaxT = 8 tasks and keeps BB accumulators per
+//     task in registers: K = 16 kMaxT / chunks angles per unit.  Per unit the block table
+//     counts, for every chunk, the blocks it touches; chunks touching none are dropped
+//     (their bins written as 0) and the rest dealt to the 16 warps by that cost in snake
+//     order.  A warp's next task descriptor is loaded one task ahead.
 //   * Decoupled pipeline: no per-block barrier.  The last warp to finish a staged block
 //     (shared-memory counter) refills its buffer with the block nbuf ahead, so warps drift
 //     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
 //   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset (split precision,
 //     DESIGN.md §5), 3 hat weights, 3 LDS.BB (the third skipped when its weight is 0) issued
-//     one line ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
+//     kAhead = 2 lines ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
 //     summed into a partial before it is added to the running total (two-level summation).
 //     A chunk skips a block none of its 32 bins sees.
 //   * Unit end: a whole unit's sums are complete in registers -> p; for the MC job also
