@@ -66,6 +66,9 @@ GEOMS = [  # (N, n_det, n_full, fft_len, B, m)
     (50, 71, 20, 0, 3, 5),         # ragged tile, odd batch (BB = 1)
     (40, 57, 12, 0, 4, 12),        # m = n_full (full EI), BB = 4
     (33, 47, 9, 0, 2, 1),          # odd N, single angle
+    (64, 40, 16, 0, 6, 4),         # truncated even detector (corner pixels' taps dropped, R18), BB = 2
+    (48, 200, 24, 0, 4, 6),        # detector far wider than the image (idle chunks)
+    (16, 1, 8, 0, 1, 3),           # a single detector bin
 ]
 
 
