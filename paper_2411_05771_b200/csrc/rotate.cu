@@ -87,17 +87,26 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
                 // split-precision source coordinates: the tile origin's source position
                 // (fp64, sRot) plus an fp32 offset of at most 2 x 32 pixels
                 const float dr = (float)rr, dc = (float)tc;
+                float fa = 0.f, fb = 0.f;
+                int ci = 0, ri = 0;
+                bool okr0 = false, okr1 = false, okc0 = false, okc1 = false;
 #pragma unroll
                 for (int b = 0; b < BB; ++b) {
                     if (b0 + b >= a.B) continue;
-                    const RotOrigin o = sRot[job.g_stride ? b : 0];
-                    const float cl = o.fc + fmaf(dc, o.cg, -dr * o.sg);
-                    const float rl = o.fr + fmaf(dc, o.sg, dr * o.cg);
-                    const float flc = floorf(cl), flr = floorf(rl);
-                    const float fb = cl - flc, fa = rl - flr;
-                    const int ci = o.bc + (int)flc, ri = o.br + (int)flr;
-                    const bool okr0 = ri >= 0 && ri < n, okr1 = ri + 1 >= 0 && ri + 1 < n;
-                    const bool okc0 = ci >= 0 && ci < n, okc1 = ci + 1 >= 0 && ci + 1 < n;
+                    if (b == 0 || job.g_stride) {  // a shared g: the BB images share the taps
+                        const RotOrigin o = sRot[job.g_stride ? b : 0];
+                        const float cl = o.fc + fmaf(dc, o.cg, -dr * o.sg);
+                        const float rl = o.fr + fmaf(dc, o.sg, dr * o.cg);
+                        const float flc = floorf(cl), flr = floorf(rl);
+                        fb = cl - flc;
+                        fa = rl - flr;
+                        ci = o.bc + (int)flc;
+                        ri = o.br + (int)flr;
+                        okr0 = ri >= 0 && ri < n;
+                        okr1 = ri + 1 >= 0 && ri + 1 < n;
+                        okc0 = ci >= 0 && ci < n;
+                        okc1 = ci + 1 >= 0 && ci + 1 < n;
+                    }
                     const float *xb = job.x + (b0 + b) * nn + (long)ri * n + ci;
                     float acc = 0.f;
                     if (okr0 && okc0) acc = fmaf((1.f - fa) * (1.f - fb), __ldg(xb), acc);
