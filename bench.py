@@ -514,7 +514,11 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(it, events):
+    def step(it, events, fused=True):
+        if fused:  # the timed form: one call, the draw overlapped with packing x1
+            sk.sketched_pass_draw(plan, x1, y, args.seed, it, m, mode, shared, rank * B, g=gbuf,
+                                  idx=ibuf, out=out, ws=ws, events=events)
+            return
         sk.draw_device(args.seed, it, rank * B, 1 if shared else B, shared, cfg.n_full, m, mode,
                        g=gbuf, idx=ibuf)
         sk.sketched_pass_profiled(plan, x1, y, gbuf, ibuf, events, out, ws)
@@ -538,14 +542,15 @@ def main():
     torch.cuda.synchronize()
     cap = torch.cuda.Stream(dev)
 
-    def capture(it, events):
+    def capture(it, events, fused=True):
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr, stream=cap):
-            step(it, events)
+            step(it, events, fused)
         return gr
 
     graphs = [capture(i * world + rank, fwd_events[i]) for i in range(n_iter)]
-    brk_graphs = [capture((n_iter + i) * world + rank, brk_events[i]) for i in range(n_brk)]
+    # the breakdown graphs launch the draw and the pass separately (each stage alone)
+    brk_graphs = [capture((n_iter + i) * world + rank, brk_events[i], False) for i in range(n_brk)]
     torch.cuda.synchronize()
     for i in range(args.warmup):
         graphs[i].replay()

@@ -313,6 +313,28 @@ skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1
                                const skei_pass_outputs *out, void *ws, size_t ws_bytes,
                                void *const *events, int32_t n_events, skei_stream stream);
 
+/* The whole of Algorithm 1 steps 2-6 in one call: the device draw
+ * a1 (skei_draw_device's draws, bit-identical to skei_draw) followed by skei_pass with
+ * x3 = NULL on those draws.  The rotation-and-packing launch is programmatically
+ * serialised behind the draw kernel, so packing x1 overlaps the draw (only the rotation of
+ * x1 waits for g).  draw->shared = 1: one draw for the batch (g_dev[1], idx_dev[1][m]);
+ * 0: a draw per image image0 + b (g_dev[B], idx_dev[B][m]); both device buffers are
+ * written by the call and read by the rest of the pass.  events: NULL, or n_events >= 6
+ * stage events as in skei_pass_profiled (event 0 before the draw).  Results are identical
+ * to skei_draw_device + skei_pass.  Errors: SKEI_ERR_ARG (NULL plan, draw, g_dev,
+ * idx_dev; shared not 0/1; events with n_events < 6), SKEI_ERR_SHAPE (B < 1, m < 1,
+ * m > n_full), SKEI_ERR_CONFIG (mode, divisibility), else as skei_pass. */
+typedef struct {
+    uint64_t seed, iter, image0;  /* the draw's key (R5); image0 unused when shared */
+    int32_t shared;               /* 1: shared per pass, 0: per image */
+    int32_t mode;                 /* 0 interleaved, 1 uniform */
+} skei_draw_spec;
+skei_status skei_pass_draw(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                           const skei_draw_spec *draw, int32_t m, int32_t *g_dev,
+                           int32_t *idx_dev, const skei_pass_outputs *out, void *ws,
+                           size_t ws_bytes, void *const *events, int32_t n_events,
+                           skei_stream stream);
+
 /* Diagnostic: shared-memory read bandwidth probe (the roofline denominator of the
  * gather kernels).  Launches `blocks` CTAs of 1024 threads that each
  * stream LDS.128 over a 32 KB shared buffer `iters` times; `sink` (device, >= blocks

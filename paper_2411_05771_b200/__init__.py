@@ -27,7 +27,7 @@ import torch
 __all__ = [
     "Plan", "SkeiError", "lib", "lib_path", "draw", "draw_device", "rotate", "radon_fwd",
     "radon_adj", "ramp_filter", "fbp", "ei_residual", "sketched_pass", "sketched_pass_host",
-    "sketched_pass_profiled", "smem_probe", "alloc_pass_outputs",
+    "sketched_pass_profiled", "sketched_pass_draw", "smem_probe", "alloc_pass_outputs",
     "workspace_bytes", "MODE_INTERLEAVED", "MODE_UNIFORM", "SHARED_IMAGE", "version",
 ]
 
@@ -51,6 +51,11 @@ class _Geom(ctypes.Structure):
 
 class _PassOut(ctypes.Structure):
     _fields_ = [(k, ctypes.c_void_p) for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad", "mc", "ei")]
+
+
+class _DrawSpec(ctypes.Structure):  # skei_draw_spec
+    _fields_ = [("seed", ctypes.c_uint64), ("iter", ctypes.c_uint64), ("image0", ctypes.c_uint64),
+                ("shared", ctypes.c_int32), ("mode", ctypes.c_int32)]
 
 
 def lib():
@@ -96,6 +101,8 @@ def lib():
                                 ctypes.POINTER(_PassOut), vp, vp, vp, sz, vp], st),
             "skei_pass_profiled": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.POINTER(_PassOut),
                                     vp, sz, ctypes.POINTER(vp), i32, vp], st),
+            "skei_pass_draw": ([vp, i32, vp, vp, ctypes.POINTER(_DrawSpec), i32, vp, vp,
+                                ctypes.POINTER(_PassOut), vp, sz, ctypes.POINTER(vp), i32, vp], st),
             "skei_smem_probe": ([vp, i32, i32, vp], st),
             "skei_version": ([], ctypes.c_char_p),
         }
@@ -435,6 +442,45 @@ def sketched_pass_profiled(plan: Plan, x1, y, g, idx, events, out: dict, ws: tor
                                     ctypes.byref(po), _ptr(ws, torch.uint8, "ws"), ws.numel(), ev,
                                     len(events), _stream(x1)), "skei_pass_profiled")
     return out
+
+
+def _events_arg(events):
+    if events is None:
+        return None, 0
+    for e in events:  # torch creates the cudaEvent_t lazily, on its first record()
+        if e is not None and e.cuda_event == 0:
+            e.record()
+    ev = (ctypes.c_void_p * len(events))(*[ctypes.c_void_p(e.cuda_event if e is not None else 0)
+                                            for e in events])
+    return ev, len(events)
+
+
+def sketched_pass_draw(plan: Plan, x1, y, seed: int, it: int, m: int, mode: int = MODE_UNIFORM,
+                       shared: bool = True, image0: int = 0, g: torch.Tensor | None = None,
+                       idx: torch.Tensor | None = None, out: dict | None = None,
+                       ws: torch.Tensor | None = None, events=None):
+    """skei_pass_draw: the device draw (a1) and the pass on it in one call; the draw is
+    written to g [1 or B] and idx [1 or B, m].  events: None or >= 6 stage events as in
+    sketched_pass_profiled (event 0 before the draw).  Returns (out, g, idx)."""
+    B = x1.shape[0]
+    nd = 1 if shared else B
+    if g is None:
+        g = torch.empty(nd, dtype=torch.int32, device=x1.device)
+    if idx is None:
+        idx = torch.empty(nd, m, dtype=torch.int32, device=x1.device)
+    if g.numel() != nd or idx.numel() != nd * m:
+        raise SkeiError(f"g, idx: expected [{nd}] and [{nd}, {m}]")
+    out = alloc_pass_outputs(plan, B, m, x1.device) if out is None else out
+    ws = plan.workspace(B, m) if ws is None else ws
+    po = _pass_out(out)
+    spec = _DrawSpec(int(seed), int(it), int(image0), int(bool(shared)), int(mode))
+    ev, nev = _events_arg(events)
+    _check(lib().skei_pass_draw(plan.handle, B, _ptr(x1, name="x1"), _ptr(y, name="y"),
+                                ctypes.byref(spec), m, _ptr(g, torch.int32, "g"),
+                                _ptr(idx, torch.int32, "idx"), ctypes.byref(po),
+                                _ptr(ws, torch.uint8, "ws"), ws.numel(), ev, nev, _stream(x1)),
+           "skei_pass_draw")
+    return out, g, idx
 
 
 def smem_probe(blocks: int, iters: int, sink: torch.Tensor):

@@ -525,7 +525,7 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
                      const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
                      int32_t idx_stride, const float *x3_in, const skei_pass_outputs *o,
                      void *ws, size_t ws_bytes, cudaEvent_t const *ev, cudaStream_t s,
-                     const ReiNoise *rei = nullptr) {
+                     const ReiNoise *rei = nullptr, const skei_draw_spec *draw = nullptr) {
     skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
     if (st != SKEI_OK) return st;
     if (!x1 || !y || !g_deg || !o || !ws) return SKEI_ERR_ARG;
@@ -551,13 +551,19 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     const float fbp_scale = (float)(M_PI / (2.0 * m));
 
     SKEI_CUDA(mark(0));
+    // a1 (skei_pass_draw): the draw kernel, followed programmatically by rotate + pack, whose
+    // x1 packing overlaps the draw (only the rotation job waits for g)
+    if (draw)
+        SKEI_CUDA(launch_draw(draw->seed, draw->iter, draw->image0, draw->shared ? 1 : B,
+                              draw->shared, plan->n_full, m, draw->mode,
+                              const_cast<int32_t *>(g_deg), const_cast<int32_t *>(idx), s));
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
     // a2: x2 = T_g x1, fused with packing x1 and x2 for the forward projector (and zeroing
     // the completion counters of the fused reductions below)
     RotPackJob rj[2] = {
         {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), ctr},
         {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), nullptr}};
-    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s));
+    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s, draw != nullptr));
     SKEI_CUDA(mark(1));
     // a3 + a7 (MC part): p1 = A_S x1 with r = p1 - y_S and mc = ||r||^2 fused into its
     // epilogue, and p2 = A_S x2, in one launch
@@ -624,6 +630,24 @@ skei_status skei_pass_profiled(const skei_plan *plan, int32_t B, const float *x1
     if (!events || n_events < 6) return SKEI_ERR_ARG;
     return run_pass(plan, B, x1, y, g_deg, g_stride, idx, m, idx_stride, nullptr, out, ws,
                     ws_bytes, (cudaEvent_t const *)events, (cudaStream_t)stream);
+}
+
+skei_status skei_pass_draw(const skei_plan *plan, int32_t B, const float *x1, const float *y,
+                           const skei_draw_spec *draw, int32_t m, int32_t *g_dev,
+                           int32_t *idx_dev, const skei_pass_outputs *out, void *ws,
+                           size_t ws_bytes, void *const *events, int32_t n_events,
+                           skei_stream stream) {
+    if (!plan || !draw || !g_dev || !idx_dev) return SKEI_ERR_ARG;
+    if (events && n_events < 6) return SKEI_ERR_ARG;
+    if (B < 1) return SKEI_ERR_SHAPE;
+    if (draw->shared != 0 && draw->shared != 1) return SKEI_ERR_ARG;
+    const int n_full = plan->n_full;
+    if (m < 1 || m > n_full) return SKEI_ERR_SHAPE;
+    if (draw->mode != 0 && draw->mode != 1) return SKEI_ERR_CONFIG;
+    if (draw->mode == 0 && n_full % m != 0) return SKEI_ERR_CONFIG;
+    const int stride = draw->shared ? 0 : 1;
+    return run_pass(plan, B, x1, y, g_dev, stride, idx_dev, m, stride ? m : 0, nullptr, out, ws,
+                    ws_bytes, (cudaEvent_t const *)events, (cudaStream_t)stream, nullptr, draw);
 }
 
 skei_status skei_smem_probe(float *sink, int32_t blocks, int32_t iters, skei_stream stream) {

@@ -33,6 +33,9 @@ __host__ __device__ inline int draw_rotation(uint64_t seed, uint64_t iter, uint6
 __global__ void __launch_bounds__(32) k_draw(uint64_t seed, uint64_t iter, uint64_t image0,
                                              int shared, int n_full, int m, int mode,
                                              int32_t *g_out, int32_t *idx_out) {
+    // let a programmatically serialized successor (the pass's rotate + pack, skei_pass_draw)
+    // start now: it waits for this grid's completion before it reads the draw
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     extern __shared__ int sm[];
     int *perm = sm;           // [n_full]
     int *tgt = sm + n_full;   // [m]

@@ -64,9 +64,10 @@ struct RotPackArgs {
     RotPackJob job[2];
     const double2 *rot;  // plan->d_rot
     int n, B, nblk, tiles_c;
+    int pdl;             // launched programmatically behind k_draw: the rotation job waits
 };
 cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
-                               int bb, cudaStream_t s);
+                               int bb, cudaStream_t s, bool pdl = false);
 cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
                           const int32_t *g, int g_stride, cudaStream_t s);
 // out = T_g^T y (gather form of the rotation's transpose)

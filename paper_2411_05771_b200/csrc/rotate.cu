@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     const long nn = (long)n * n;
     if (job.zero && blockIdx.x == 0 && blockIdx.y == 0)  // the pass's counters (fused
         for (int t = threadIdx.x; t < kPassCounters; t += blockDim.x) job.zero[t] = 0u;  // reductions, forward split units)
+    // launched programmatically behind the pass's own k_draw (skei_pass_draw): only the
+    // rotation job reads the draw (g), so only its blocks wait for the draw grid; the
+    // packing of x1 runs while the draw is still in flight
+    if (a.pdl && job.g != nullptr) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (job.g != nullptr && threadIdx.x < BB && b0 + (int)threadIdx.x < a.B) {
         // source position of the tile origin (r0, c0) for image b0 + threadIdx.x, in fp64:
         // c' = h + (c0 - h) cos g + (h - r0) sin g,  r' = h + (c0 - h) sin g - (h - r0) cos g
@@ -252,8 +256,9 @@ size_t pack_floats(const skei_plan *plan, int B, int bb) {
 }
 
 cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
-                               int bb, cudaStream_t s) {
+                               int bb, cudaStream_t s, bool pdl) {
     RotPackArgs a;
+    a.pdl = pdl ? 1 : 0;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
     a.n = plan->n;
@@ -266,12 +271,22 @@ cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, in
     a.tiles_c = (side + kT - 1) / kT;
     dim3 grid((unsigned)(a.tiles_c * a.tiles_c), (unsigned)((B + bb - 1) / bb), (unsigned)njobs);
     const bool xm = a.job[0].xm || (njobs > 1 && a.job[1].xm);
+    // pdl: programmatic stream serialization (the kernel may start once the previous grid,
+    // the pass's k_draw, has triggered; the rotation job waits for its completion)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
 #define SKEI_ROTPACK(BBV)                                                       \
     do {                                                                        \
-        if (xm)                                                                 \
-            k_rotate_pack<BBV, true><<<grid, kThreads, 0, s>>>(a);              \
-        else                                                                    \
-            k_rotate_pack<BBV, false><<<grid, kThreads, 0, s>>>(a);             \
+        cudaError_t e_ = xm ? cudaLaunchKernelEx(&cfg, k_rotate_pack<BBV, true>, a)  \
+                            : cudaLaunchKernelEx(&cfg, k_rotate_pack<BBV, false>, a); \
+        if (e_ != cudaSuccess) return e_;                                       \
     } while (0)
     switch (bb) {
         case 4: SKEI_ROTPACK(4); break;

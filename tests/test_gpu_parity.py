@@ -261,6 +261,46 @@ def test_pass_backprojections_match_standalone_calls(name):
     assert torch.equal(sk.radon_adj(plan, out["r"], idx, 2.0), out["grad"])
 
 
+@pytest.mark.parametrize("name,shared,mode", [("cfg2", True, sk.MODE_UNIFORM),
+                                              ("cfg2", True, sk.MODE_INTERLEAVED),
+                                              ("cfg3", True, sk.MODE_UNIFORM),
+                                              ("cfg2", False, sk.MODE_UNIFORM)])
+def test_pass_draw_matches_draw_then_pass(name, shared, mode):
+    """skei_pass_draw (draw kernel + programmatically serialised rotate/pack) gives exactly
+    the draws of skei_draw_device and the outputs of skei_pass on them, also when captured
+    into a CUDA graph and replayed (the bench's timed form)."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = (dev(a) for a in synth.make_workload(cfg))
+    nd = 1 if shared else cfg.B
+    g, idx = sk.draw_device(7, 11, 3, nd, shared, cfg.n_full, cfg.m, mode)
+    ref = sk.sketched_pass(plan, x1, y, g, idx)
+    out, g2, idx2 = sk.sketched_pass_draw(plan, x1, y, 7, 11, cfg.m, mode, shared, 3)
+    assert torch.equal(g, g2) and torch.equal(idx, idx2)
+    for k in ref:
+        assert torch.equal(out[k], ref[k]), k
+    # graph capture and replay, outputs cleared in between
+    for v in out.values():
+        v.zero_()
+    g2.zero_()
+    idx2.zero_()
+    ws = plan.workspace(cfg.B, cfg.m)
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=cap):
+        sk.sketched_pass_draw(plan, x1, y, 7, 11, cfg.m, mode, shared, 3, g=g2, idx=idx2,
+                              out=out, ws=ws)
+    for v in out.values():
+        v.zero_()
+    for _ in range(2):
+        gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(g, g2) and torch.equal(idx, idx2)
+    for k in ref:
+        assert torch.equal(out[k], ref[k]), f"graph {k}"
+
+
 def test_gpu_adjoint_identity():
     cfg = synth.CONFIGS["cfg2"]
     plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
