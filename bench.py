@@ -660,10 +660,13 @@ def main():
             t = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        h2d = hx1.numel() * 4 + hy.numel() * 4 + ng * 4 + ng * m * 4
+        # a shared sketch copies only y's m sketched rows (skei_pass_host), else all of y
+        y_h2d = B * m * cfg.n_det * 4 if shared else hy.numel() * 4
+        h2d = hx1.numel() * 4 + y_h2d + ng * 4 + ng * m * 4
         e2e = {"value": world * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(2 * B * 4),
-               "timing": "host wall clock over all steps; per step: host draw, H2D of x1/y/g/idx "
+               "timing": "host wall clock over all steps; per step: host draw, H2D of x1, y_S "
+                         "(the sketched rows of y; all of y for per-image sketches), g, idx "
                          "from pinned memory, the pass, D2H of mc/ei, in-stream L2 flush (256 MB "
                          "write) behind it; two streams alternate so one step's H2D overlaps "
                          "the previous step's pass"}

@@ -276,9 +276,14 @@ skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const f
 /* End-to-end variant from HOST buffers: copies host x1 [B][n][n], host y
  * [B][n_full][n_det], host g [B or 1] and host idx into the caller's device
  * buffers (d_x1, d_y, d_g, d_idx, same shapes), runs skei_pass, and copies
- * mc/ei back into host h_mc[B], h_ei[B].  Host buffers should be pinned for the
- * copies to be asynchronous.  The caller synchronises `stream` before reading
- * h_mc / h_ei. */
+ * mc/ei back into host h_mc[B], h_ei[B].  With one sketch for the batch
+ * (idx_stride 0) only the m sketched rows of y are copied — one strided copy per
+ * run of consecutive angle indices — into the head of d_y as y_S [B][m][n_det]
+ * (the pass only reads y_S, Alg. 1 step 6); per-image sketches copy all of y.
+ * Results are identical to skei_pass on device copies.  Host buffers should be
+ * pinned for the copies to be asynchronous.  The caller synchronises `stream`
+ * before reading h_mc / h_ei.  Errors: as skei_pass; SKEI_ERR_ARG if a host
+ * angle index is outside [0, n_full). */
 skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const float *h_y, const int32_t *h_g, int32_t g_stride,
                            const int32_t *h_idx, int32_t m, int32_t idx_stride,

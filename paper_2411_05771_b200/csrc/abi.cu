@@ -525,7 +525,8 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
                      const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
                      int32_t idx_stride, const float *x3_in, const skei_pass_outputs *o,
                      void *ws, size_t ws_bytes, cudaEvent_t const *ev, cudaStream_t s,
-                     const ReiNoise *rei = nullptr, const skei_draw_spec *draw = nullptr) {
+                     const ReiNoise *rei = nullptr, const skei_draw_spec *draw = nullptr,
+                     bool y_sketched = false) {
     skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
     if (st != SKEI_OK) return st;
     if (!x1 || !y || !g_deg || !o || !ws) return SKEI_ERR_ARG;
@@ -571,7 +572,7 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     // padded layout (its windows are then one bulk copy per angle)
     const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
     float *qi = il ? ws_f(ws, wl.qi) : nullptr, *ri = il ? ws_f(ws, wl.ri) : nullptr;
-    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1, y, o->r},
+    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1, y, o->r, y_sketched},
                     {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
     FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
@@ -672,13 +673,33 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
     cudaStream_t s = (cudaStream_t)stream;
     const size_t nn = (size_t)plan->n * plan->n, ny = (size_t)plan->n_full * plan->n_det;
     SKEI_CUDA(cudaMemcpyAsync(d_x1, h_x1, sizeof(float) * B * nn, cudaMemcpyHostToDevice, s));
-    SKEI_CUDA(cudaMemcpyAsync(d_y, h_y, sizeof(float) * B * ny, cudaMemcpyHostToDevice, s));
+    const int n_det = plan->n_det;
+    for (long i = 0; i < (long)m * (idx_stride ? B : 1); ++i)  // host indices: checked here
+        if (h_idx[i] < 0 || h_idx[i] >= plan->n_full) return SKEI_ERR_ARG;
+    // With one sketch for the batch only the m sketched rows of y cross the link: each run
+    // of consecutive angle indices is one strided copy of B row blocks, into d_y as y_S
+    // [B][m][n_det] (the pass then reads y_S row k for angle idx[k]).  Per-image sketches
+    // copy the whole of y.
+    const bool y_sk = idx_stride == 0;
+    if (y_sk) {
+        for (int k = 0; k < m;) {
+            int e = k + 1;
+            while (e < m && h_idx[e] == h_idx[e - 1] + 1) ++e;
+            SKEI_CUDA(cudaMemcpy2DAsync(d_y + (size_t)k * n_det, sizeof(float) * m * n_det,
+                                        h_y + (size_t)h_idx[k] * n_det, sizeof(float) * ny,
+                                        sizeof(float) * (e - k) * n_det, B,
+                                        cudaMemcpyHostToDevice, s));
+            k = e;
+        }
+    } else {
+        SKEI_CUDA(cudaMemcpyAsync(d_y, h_y, sizeof(float) * B * ny, cudaMemcpyHostToDevice, s));
+    }
     SKEI_CUDA(cudaMemcpyAsync(d_g, h_g, sizeof(int32_t) * (g_stride ? B : 1),
                               cudaMemcpyHostToDevice, s));
     SKEI_CUDA(cudaMemcpyAsync(d_idx, h_idx, sizeof(int32_t) * (size_t)m * (idx_stride ? B : 1),
                               cudaMemcpyHostToDevice, s));
-    st = skei_pass(plan, B, d_x1, d_y, d_g, g_stride, d_idx, m, idx_stride, nullptr, o, ws,
-                   ws_bytes, stream);
+    st = run_pass(plan, B, d_x1, d_y, d_g, g_stride, d_idx, m, idx_stride, nullptr, o, ws,
+                  ws_bytes, nullptr, s, nullptr, nullptr, y_sk);
     if (st != SKEI_OK) return st;
     SKEI_CUDA(cudaMemcpyAsync(h_mc, o->mc, sizeof(float) * B, cudaMemcpyDeviceToHost, s));
     SKEI_CUDA(cudaMemcpyAsync(h_ei, o->ei, sizeof(float) * B, cudaMemcpyDeviceToHost, s));

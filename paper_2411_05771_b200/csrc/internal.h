@@ -81,6 +81,7 @@ struct FwdJob {
     float *p;
     const float *y;  // full sinogram [B][n_full][n_det] or NULL (job 0 only)
     float *r;        // residual [B][m][n_det] or NULL
+    int y_sketched = 0;  // y holds only the sketched rows, [B][m][n_det] (row k = angle idx[k])
 };
 struct FwdMc {
     float *part;    // [B][fwd_mc_slots] partial sums

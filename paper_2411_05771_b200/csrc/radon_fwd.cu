@@ -590,10 +590,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #pragma unroll
             for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
             if (mc) {
-                const long yj = (long)idx[slot] * n_det + j;
+                const long yj = (long)(job.y_sketched ? slot : idx[slot]) * n_det + j;
+                const long ys = (long)(job.y_sketched ? a.m : n_full) * n_det;
 #pragma unroll
                 for (int b = 0; b < BB; ++b) {
-                    const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * n_full * n_det + yj);
+                    const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * ys + yj);
                     if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
                     racc[b] = fmaf(dr, dr, racc[b]);
                 }

@@ -313,26 +313,36 @@ def test_gpu_adjoint_identity():
     assert abs(lhs - rhs) / (np.linalg.norm(Ax) * np.linalg.norm(yv)) <= 1e-6
 
 
-def test_pass_host_matches_device_pass():
-    cfg = synth.CONFIGS["cfg1"]
+@pytest.mark.parametrize("name,shared,mode", [("cfg1", True, sk.MODE_UNIFORM),
+                                              ("cfg2", True, sk.MODE_UNIFORM),
+                                              ("cfg2", True, sk.MODE_INTERLEAVED),
+                                              ("cfg2", False, sk.MODE_UNIFORM)])
+def test_pass_host_matches_device_pass(name, shared, mode):
+    """skei_pass_host (a shared sketch copies only y's sketched rows, as strided copies of
+    runs of consecutive angles) gives exactly skei_pass's results on device copies."""
+    cfg = synth.CONFIGS[name]
     plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
     x1, y = synth.make_workload(cfg)
-    g, idx = sk.draw(0, 0, SH, cfg.n_full, cfg.m)
-    ref = sk.sketched_pass(plan, dev(x1), dev(y), idx_t([g]), idx_t(idx))
+    draws = [sk.draw(0, 0, SH if shared else b, cfg.n_full, cfg.m, mode)
+             for b in range(1 if shared else cfg.B)]
+    g = [d[0] for d in draws]
+    idx = np.stack([d[1] for d in draws])
+    ref = sk.sketched_pass(plan, dev(x1), dev(y), idx_t(g), idx_t(idx))
     h = {k: torch.from_numpy(v).pin_memory() for k, v in (("x1", x1), ("y", y))}
-    hg = torch.tensor([g], dtype=torch.int32).pin_memory()
+    hg = torch.tensor(g, dtype=torch.int32).pin_memory()
     hidx = torch.tensor(idx, dtype=torch.int32).pin_memory()
     d = sk.alloc_pass_outputs(plan, cfg.B, cfg.m, "cuda")
-    d.update(x1=torch.empty_like(dev(x1)), y=torch.empty_like(dev(y)),
-             g=torch.empty(1, dtype=torch.int32, device="cuda"),
-             idx=torch.empty(cfg.m, dtype=torch.int32, device="cuda"))
+    d.update(x1=torch.empty_like(dev(x1)), y=torch.full_like(dev(y), float("nan")),
+             g=torch.empty(len(g), dtype=torch.int32, device="cuda"),
+             idx=torch.empty(idx.shape, dtype=torch.int32, device="cuda"))
     hmc = torch.empty(cfg.B).pin_memory()
     hei = torch.empty(cfg.B).pin_memory()
     ws = plan.workspace(cfg.B, cfg.m)
     sk.sketched_pass_host(plan, h["x1"], h["y"], hg, hidx, d, hmc, hei, ws, d["x2"])
     torch.cuda.synchronize()
     assert torch.equal(hmc, ref["mc"].cpu()) and torch.equal(hei, ref["ei"].cpu())
-    assert torch.equal(d["grad"], ref["grad"])
+    for k in ("r", "grad", "xfbp", "p1"):
+        assert torch.equal(d[k], ref[k]), k
 
 
 def test_invalid_shapes_raise():
