@@ -182,10 +182,11 @@ skei_status skei_plan_create(const skei_geometry *geom, int device, skei_plan **
     for (int ip = 0; ip < npass; ++ip)
         for (int k = 0; k < ns[ip]; ++k)
             for (int r = 0; r < radix[ip]; ++r) {
-                // exp(-2 pi i r k / (R Ns)), reduced exactly before the fp64 trig
+                // exp(-2 pi i r k / (R Ns)), reduced exactly before the fp64 trig; r-major,
+                // so the threads of a warp (consecutive k) load consecutive entries
                 const long num = ((long)r * k) % ((long)radix[ip] * ns[ip]);
                 const double a = 2.0 * M_PI * (double)num / ((double)radix[ip] * ns[ip]);
-                tw[twoff[ip] + k * radix[ip] + r] = make_float2((float)std::cos(a), (float)(-std::sin(a)));
+                tw[twoff[ip] + r * ns[ip] + k] = make_float2((float)std::cos(a), (float)(-std::sin(a)));
             }
 
     skei_plan *p = new skei_plan();

@@ -16,7 +16,7 @@ struct skei_plan {
     double2 *d_trig;  // [n_full] (cos, sin) of theta_i = i*pi/n_full, fp64
     float *d_ramp;    // [fft_len] R[k] / P, fp32 (from an fp64 DFT)
     // FFT pass plan (ramp.cu): radix, sub-transform length Ns and twiddle-table offset per
-    // pass; d_twp[off + k R + r] = exp(-2 pi i r k / (R Ns)), fp32 rounded from fp64
+    // pass; d_twp[off + r Ns + k] = exp(-2 pi i r k / (R Ns)), fp32 rounded from fp64
     int fft_npass, fft_radix[kMaxFftPass], fft_ns[kMaxFftPass], fft_twoff[kMaxFftPass];
     float2 *d_twp;
     double2 *d_rot;   // [360] (cos g, sin g) of g degrees, fp64, exact at multiples of 90

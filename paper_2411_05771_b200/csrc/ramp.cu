@@ -150,11 +150,12 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
     for (int jj = 0; jj < J; ++jj) {
         const int j = threadIdx.x + jj * blockDim.x;
         const int k = j & (Ns - 1);
-        if (Ns > 1) {
-            const float2 *t = tw + (long)k * R;
+        if (Ns > 1) {  // twiddles r-major: a warp's consecutive k load consecutive entries
+            const float2 *t = tw + k;
 #pragma unroll
             for (int r = 1; r < R; ++r)
-                v[jj][r] = inverse ? cmulc(v[jj][r], __ldg(t + r)) : cmul(v[jj][r], __ldg(t + r));
+                v[jj][r] = inverse ? cmulc(v[jj][r], __ldg(t + (long)r * Ns))
+                                   : cmul(v[jj][r], __ldg(t + (long)r * Ns));
         }
         dft<R>(v[jj], inverse);
         const int d = (j - k) * R + k;
