@@ -36,6 +36,7 @@ constexpr int kThreads = 256;  // 8 warps: warp = 8 rows x 8 columns (4 pixel pa
 constexpr int kPairs = 1;      // pixel pairs per thread
 constexpr int kKC = 12;        // angles per staged chunk (2 buffers x 2 jobs fit 48 KB)
 constexpr int kW = 40;         // staged bins per angle (>= sqrt(31^2 + 15^2) + 3)
+constexpr int kTab = 256;      // m <= kTab: the whole per-angle table is built up front
 
 struct AdjArgs {
     AdjJob job[2];
@@ -107,8 +108,10 @@ __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
 template <int BB, int NJ, bool BULK>
 __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     __shared__ __align__(128) float win[2][NJ][kKC * kW * BB];
-    __shared__ float s_off[2][kKC], s_cos[2][kKC], s_sin[2][kKC];
-    __shared__ int s_w0[2][kKC];
+    // per-angle table: entry k of the sketch at [k] when m <= kTab (built once, by all
+    // threads), else entry t of chunk ch at [(ch & 1) * kKC + t] (built per chunk)
+    __shared__ float s_off[kTab], s_cos[kTab], s_sin[kTab];
+    __shared__ int s_w0[kTab];
     __shared__ float s_red[kThreads / 32][BB];
     __shared__ bool s_last;
     __shared__ __align__(8) uint64_t full[2];  // BULK: window copies of each buffer landed
@@ -145,22 +148,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         }
         __syncthreads();
     }
-    // per-angle table of chunk ch (threads < kKC): window origin, fp64 -> split precision
-    auto table = [&](int ch, int bf) {
+    const bool full_tab = a.m <= kTab;
+    // table entry of sketch angle k at slot e: window origin, fp64 -> split precision
+    auto entry = [&](int k, int e) {
+        const double2 cs = a.g.trig[idx[k]];
+        // detector position of the tile origin pixel (tr0, tc0), fp64
+        const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
+        const double jmin = J0 + fmin(0.0, (kTileW - 1) * cs.x) + fmin(0.0, -(kTileH - 1) * cs.y);
+        const double w0 = floor(jmin);
+        s_off[e] = (float)(J0 - w0);
+        s_cos[e] = (float)cs.x;
+        s_sin[e] = (float)cs.y;
+        s_w0[e] = (int)w0;
+    };
+    // table slot of chunk ch's first angle
+    auto tbase = [&](int ch) { return full_tab ? ch * kKC : (ch & 1) * kKC; };
+    // per-angle table of chunk ch (threads < kKC; nothing to do for a whole-sketch table)
+    auto table = [&](int ch) {
         const int k0 = ch * kKC;
         const int kc = min(kKC, a.m - k0);
-        if (threadIdx.x < kc) {
-            const double2 cs = a.g.trig[idx[k0 + threadIdx.x]];
-            // detector position of the tile origin pixel (tr0, tc0), fp64
-            const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
-            const double jmin = J0 + fmin(0.0, (kTileW - 1) * cs.x) + fmin(0.0, -(kTileH - 1) * cs.y);
-            const double w0 = floor(jmin);
-            s_off[bf][threadIdx.x] = (float)(J0 - w0);
-            s_cos[bf][threadIdx.x] = (float)cs.x;
-            s_sin[bf][threadIdx.x] = (float)cs.y;
-            s_w0[bf][threadIdx.x] = (int)w0;
-        }
+        if (!full_tab && threadIdx.x < kc) entry(k0 + threadIdx.x, tbase(ch) + threadIdx.x);
     };
+    if (full_tab) {  // the whole table up front: one dependent-load latency per CTA
+        for (int k = threadIdx.x; k < a.m; k += kThreads) entry(k, k);
+        __syncthreads();
+    }
     // bulk path (thread 0): one bulk copy per (angle, job): kW bins x BB images, 16 B per bin,
     // from the interleaved padded sinogram (in bounds for any window origin >= -kAdjPad; the
     // pads supply the zeros outside [0, n_det)); completion on full[bf]
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         mbar_expect_tx(&full[bf], bytes * kc * NJ);
         const long wp = a.g.n_det + 2 * kAdjPad;
         for (int t = 0; t < kc; ++t) {
-            const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[bf][t];
+            const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[tbase(ch) + t];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj)
                 bulk_g2s(&win[bf][jj][t * kW * BB], a.job[jj].pi + row * BB, bytes, &full[bf]);
@@ -182,14 +194,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     auto stage = [&](int ch, int bf) {
         const int k0 = ch * kKC;
         const int kc = min(kKC, a.m - k0);
-        table(ch, bf);
+        table(ch);
         __syncthreads();  // window origins visible
         // element e -> (angle t, bin w, image b), image fastest
         for (int e = threadIdx.x; e < kc * kW * BB; e += kThreads) {
             const int b = e % BB;
             const int w = (e / BB) % kW;
             const int t = e / (BB * kW);
-            const int jb = s_w0[bf][t] + w;
+            const int jb = s_w0[tbase(ch) + t] + w;
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) {
                 float *dst = &win[bf][jj][e];
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     // (arrive.release by lane 0, try_wait.acquire by the consumers)
     auto produce = [&](int ch, int bf) {
         if (warp == 0) {
-            table(ch, bf);
+            table(ch);
             __syncwarp();
             if (lane == 0) issue_bulk(ch, bf);
         }
@@ -231,11 +243,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
             __syncthreads();
         }
         const int kc = min(kKC, a.m - ch * kKC);
+        const int tb = tbase(ch);
 #pragma unroll 2
         for (int t = 0; t < kc; ++t) {
-            const float ct = s_cos[bf][t], st = s_sin[bf][t];
+            const float ct = s_cos[tb + t], st = s_sin[tb + t];
             // position of pixel (ry, 2 pc) relative to the window origin
-            const float rowb = fmaf(-(float)ry, st, s_off[bf][t]);
+            const float rowb = fmaf(-(float)ry, st, s_off[tb + t]);
 #pragma unroll
             for (int p = 0; p < kPairs; ++p) {
                 const int c = 2 * (pc0 + 16 * p);
