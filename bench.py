@@ -37,6 +37,7 @@ UNIT = "passes/s"
 # (+ fused MC residual) | 2 | ramp | 3 | backprojection x2 (+ fused EI residual) | 4 | 5 end
 STAGES = ["rotate_pack", "radon_fwd_x2", "ramp", "radon_adj_x2"]
 LAUNCHES_PER_STEP = 5  # draw, rotate+pack, forward (2 jobs + MC), ramp, adjoint (2 jobs + EI)
+E2E_SLOTS = 3  # e2e pipeline depth (slots of device buffers and streams)
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -603,10 +604,11 @@ def main():
     ms_per_step = total_ms / args.steps
     value = world * args.steps / (total_ms * 1e-3)
 
-    # ---- end to end through the public host-buffer call (skei_pass_host).  Two slots (device
-    # inputs/outputs, workspace, pinned draw/result buffers, stream) alternate, so step i's
-    # H2D of (x1, y) on one copy engine overlaps step i-1's pass on the SMs — what a user
-    # streaming batches through the library does.  Every step still copies its own inputs
+    # ---- end to end through the public host-buffer call (skei_pass_host).  E2E_SLOTS slots
+    # (device inputs/outputs, workspace, pinned draw/staging/result buffers, stream) rotate, so
+    # step i's host preparation and H2D overlap the passes of steps i-1, i-2 on the SMs — what
+    # a user streaming batches through the library does (with two slots, a slot's next host
+    # gather + H2D could only start once its previous pass ended, idling the SMs).  Every step still copies its own inputs
     # from pinned host memory, runs the whole pass and reads its mc/ei back; the L2 is
     # flushed in-stream before every step; the clock is the host wall clock over all steps.
     e2e = None
@@ -615,7 +617,7 @@ def main():
         hy = torch.from_numpy(y_np).pin_memory()
         ng = 1 if shared else B
         slots = []
-        for _ in range(2):
+        for _ in range(E2E_SLOTS):
             d = sk.alloc_pass_outputs(plan, B, m, dev)
             d.update(x1=torch.empty_like(x1), y=torch.empty_like(y), g=torch.empty_like(gbuf),
                      idx=torch.empty_like(ibuf))
@@ -623,11 +625,12 @@ def main():
                               hg=torch.empty(ng, dtype=torch.int32).pin_memory(),
                               hidx=torch.empty(ng, m, dtype=torch.int32).pin_memory(),
                               hmc=torch.empty(B).pin_memory(), hei=torch.empty(B).pin_memory(),
+                              ys=torch.empty(B, m, cfg.n_det).pin_memory() if shared else None,
                               done=None, fl=torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)))
         results = []
 
         def e2e_step(it):
-            sl = slots[it % 2]
+            sl = slots[it % E2E_SLOTS]
             if sl["done"] is not None:  # this slot's previous step: its results are back
                 sl["done"].synchronize()
                 results.append(float(sl["hmc"][0]))
@@ -638,7 +641,7 @@ def main():
                 sl["hidx"][b] = torch.tensor(ii, dtype=torch.int32)
             with torch.cuda.stream(sl["st"]):
                 sk.sketched_pass_host(plan, hx1, hy, sl["hg"], sl["hidx"], sl["d"], sl["hmc"],
-                                      sl["hei"], sl["ws"], sl["fl"])
+                                      sl["hei"], sl["ws"], sl["fl"], h_ystage=sl["ys"])
                 # L2 flush behind the pass in the same stream (so it never holds up the next
                 # step's H2D on the other stream): this slot's next pass starts cold
                 sl["fl"].zero_()
@@ -646,7 +649,7 @@ def main():
                 ev.record(sl["st"])
             sl["done"] = ev
 
-        for i in range(4):
+        for i in range(2 * E2E_SLOTS):
             e2e_step(i)
         torch.cuda.synchronize()
         for sl in slots:
@@ -666,10 +669,11 @@ def main():
         e2e = {"value": world * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(2 * B * 4),
                "timing": "host wall clock over all steps; per step: host draw, H2D of x1, y_S "
-                         "(the sketched rows of y; all of y for per-image sketches), g, idx "
+                         "(the sketched rows of y gathered into a pinned staging buffer by the "
+                         "library; all of y for per-image sketches), g, idx "
                          "from pinned memory, the pass, D2H of mc/ei, in-stream L2 flush (256 MB "
-                         "write) behind it; two streams alternate so one step's H2D overlaps "
-                         "the previous step's pass"}
+                         "write) behind it; slots with their own streams rotate, so one step's H2D overlaps "
+                         "the previous steps' passes (3 slots)"}
 
     if rank != 0:
         if world > 1:

@@ -277,9 +277,12 @@ skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const f
  * [B][n_full][n_det], host g [B or 1] and host idx into the caller's device
  * buffers (d_x1, d_y, d_g, d_idx, same shapes), runs skei_pass, and copies
  * mc/ei back into host h_mc[B], h_ei[B].  With one sketch for the batch
- * (idx_stride 0) only the m sketched rows of y are copied — one strided copy per
- * run of consecutive angle indices — into the head of d_y as y_S [B][m][n_det]
- * (the pass only reads y_S, Alg. 1 step 6); per-image sketches copy all of y.
+ * (idx_stride 0) only the m sketched rows of y cross the link, into the head of d_y
+ * as y_S [B][m][n_det] (the pass only reads y_S, Alg. 1 step 6): if h_ystage (host,
+ * >= B*m*n_det floats, pinned) is given, the rows are gathered into it on the calling
+ * thread and sent as one copy; else one strided copy per run of consecutive angle
+ * indices.  h_ystage is rewritten at call time, so a previous call's copy from it must
+ * have completed.  Per-image sketches copy all of y (h_ystage unused, may be NULL).
  * Results are identical to skei_pass on device copies.  Host buffers should be
  * pinned for the copies to be asynchronous.  The caller synchronises `stream`
  * before reading h_mc / h_ei.  Errors: as skei_pass; SKEI_ERR_ARG if a host
@@ -289,7 +292,7 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const int32_t *h_idx, int32_t m, int32_t idx_stride,
                            float *d_x1, float *d_y, int32_t *d_g, int32_t *d_idx,
                            const skei_pass_outputs *out, float *h_mc, float *h_ei,
-                           void *ws, size_t ws_bytes, skei_stream stream);
+                           float *h_ystage, void *ws, size_t ws_bytes, skei_stream stream);
 
 /* ---------------------------- next row: the REI variant of the pass --
  * Robust EI: the EI branch reconstructs from simulated noisy measurements,

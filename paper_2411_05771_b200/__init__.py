@@ -98,7 +98,7 @@ def lib():
             "skei_pass": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, ctypes.POINTER(_PassOut),
                            vp, sz, vp], st),
             "skei_pass_host": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, vp, vp, vp, vp,
-                                ctypes.POINTER(_PassOut), vp, vp, vp, sz, vp], st),
+                                ctypes.POINTER(_PassOut), vp, vp, vp, vp, sz, vp], st),
             "skei_pass_profiled": ([vp, i32, vp, vp, vp, i32, vp, i32, i32, ctypes.POINTER(_PassOut),
                                     vp, sz, ctypes.POINTER(vp), i32, vp], st),
             "skei_pass_draw": ([vp, i32, vp, vp, ctypes.POINTER(_DrawSpec), i32, vp, vp,
@@ -488,9 +488,11 @@ def smem_probe(blocks: int, iters: int, sink: torch.Tensor):
     _check(lib().skei_smem_probe(_ptr(sink, name="sink"), blocks, iters, _stream(sink)), "skei_smem_probe")
 
 
-def sketched_pass_host(plan: Plan, h_x1, h_y, h_g, h_idx, d: dict, h_mc, h_ei, ws, stream_tensor):
-    """skei_pass_host: H2D of (x1, y, g, idx) from (pinned) host tensors into d['x1'], d['y'],
-    d['g'], d['idx'], the pass, and D2H of mc/ei into h_mc/h_ei (asynchronous)."""
+def sketched_pass_host(plan: Plan, h_x1, h_y, h_g, h_idx, d: dict, h_mc, h_ei, ws, stream_tensor,
+                       h_ystage=None):
+    """skei_pass_host: H2D of (x1, y_S or y, g, idx) from (pinned) host tensors into d['x1'],
+    d['y'], d['g'], d['idx'], the pass, and D2H of mc/ei into h_mc/h_ei (asynchronous).
+    h_ystage: optional pinned host staging tensor (>= B*m*n_det floats) for the gathered y_S."""
     B, m = h_x1.shape[0], h_idx.shape[-1]
     po = _pass_out(d)
     g_stride = 0 if h_g.numel() == 1 else 1
@@ -498,5 +500,6 @@ def sketched_pass_host(plan: Plan, h_x1, h_y, h_g, h_idx, d: dict, h_mc, h_ei, w
     hp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     _check(lib().skei_pass_host(plan.handle, B, hp(h_x1), hp(h_y), hp(h_g), g_stride, hp(h_idx), m,
                                 idx_stride, hp(d["x1"]), hp(d["y"]), hp(d["g"]), hp(d["idx"]),
-                                ctypes.byref(po), hp(h_mc), hp(h_ei), hp(ws), ws.numel(),
+                                ctypes.byref(po), hp(h_mc), hp(h_ei),
+                                hp(h_ystage) if h_ystage is not None else None, hp(ws), ws.numel(),
                                 _stream(stream_tensor)), "skei_pass_host")

@@ -662,8 +662,8 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const float *h_y, const int32_t *h_g, int32_t g_stride,
                            const int32_t *h_idx, int32_t m, int32_t idx_stride, float *d_x1,
                            float *d_y, int32_t *d_g, int32_t *d_idx,
-                           const skei_pass_outputs *o, float *h_mc, float *h_ei, void *ws,
-                           size_t ws_bytes, skei_stream stream) {
+                           const skei_pass_outputs *o, float *h_mc, float *h_ei,
+                           float *h_ystage, void *ws, size_t ws_bytes, skei_stream stream) {
     if (!plan || !h_x1 || !h_y || !h_g || !h_idx || !d_x1 || !d_y || !d_g || !d_idx || !o ||
         !h_mc || !h_ei)
         return SKEI_ERR_ARG;
@@ -682,7 +682,19 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
     // [B][m][n_det] (the pass then reads y_S row k for angle idx[k]).  Per-image sketches
     // copy the whole of y.
     const bool y_sk = idx_stride == 0;
-    if (y_sk) {
+    if (y_sk && h_ystage) {  // host gather of the sketched rows, then one copy
+        for (int b = 0; b < B; ++b)
+            for (int k = 0; k < m;) {
+                int e = k + 1;
+                while (e < m && h_idx[e] == h_idx[e - 1] + 1) ++e;
+                std::memcpy(h_ystage + ((size_t)b * m + k) * n_det,
+                            h_y + (size_t)b * ny + (size_t)h_idx[k] * n_det,
+                            sizeof(float) * (e - k) * n_det);
+                k = e;
+            }
+        SKEI_CUDA(cudaMemcpyAsync(d_y, h_ystage, sizeof(float) * B * m * n_det,
+                                  cudaMemcpyHostToDevice, s));
+    } else if (y_sk) {
         for (int k = 0; k < m;) {
             int e = k + 1;
             while (e < m && h_idx[e] == h_idx[e - 1] + 1) ++e;

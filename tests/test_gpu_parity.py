@@ -313,11 +313,12 @@ def test_gpu_adjoint_identity():
     assert abs(lhs - rhs) / (np.linalg.norm(Ax) * np.linalg.norm(yv)) <= 1e-6
 
 
+@pytest.mark.parametrize("stage", [False, True])
 @pytest.mark.parametrize("name,shared,mode", [("cfg1", True, sk.MODE_UNIFORM),
                                               ("cfg2", True, sk.MODE_UNIFORM),
                                               ("cfg2", True, sk.MODE_INTERLEAVED),
                                               ("cfg2", False, sk.MODE_UNIFORM)])
-def test_pass_host_matches_device_pass(name, shared, mode):
+def test_pass_host_matches_device_pass(name, shared, mode, stage):
     """skei_pass_host (a shared sketch copies only y's sketched rows, as strided copies of
     runs of consecutive angles) gives exactly skei_pass's results on device copies."""
     cfg = synth.CONFIGS[name]
@@ -338,7 +339,8 @@ def test_pass_host_matches_device_pass(name, shared, mode):
     hmc = torch.empty(cfg.B).pin_memory()
     hei = torch.empty(cfg.B).pin_memory()
     ws = plan.workspace(cfg.B, cfg.m)
-    sk.sketched_pass_host(plan, h["x1"], h["y"], hg, hidx, d, hmc, hei, ws, d["x2"])
+    ys = torch.full((cfg.B, cfg.m, cfg.n_det), float("nan")).pin_memory() if stage else None
+    sk.sketched_pass_host(plan, h["x1"], h["y"], hg, hidx, d, hmc, hei, ws, d["x2"], h_ystage=ys)
     torch.cuda.synchronize()
     assert torch.equal(hmc, ref["mc"].cpu()) and torch.equal(hei, ref["ei"].cpu())
     for k in ("r", "grad", "xfbp", "p1"):
