@@ -69,10 +69,15 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     }
     __syncthreads();
 
-    const int c = c0 + tc;
+    // Rotations nearer a quarter turn (|sin g| > |cos g|) map a warp's 32 lanes to 32 rows
+    // of one tile column: consecutive source positions then step by |cos g| < |sin g| rows
+    // (instead of |sin g| per column), so a warp's bilinear taps stay within a few cache
+    // lines; the plain output is then written from the staged tile (coalesced)
+    const bool swp = job.g != nullptr && fabsf(sRot[0].sg) > fabsf(sRot[0].cg);
 #pragma unroll
     for (int i = 0; i < kT / 8; ++i) {
-        const int rr = tr + 8 * i, r = r0 + rr;
+        const int rr = swp ? tc : tr + 8 * i, r = r0 + rr;
+        const int cc = swp ? tr + 8 * i : tc, c = c0 + cc;
         float v[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) v[b] = 0.f;
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
             } else {
                 // split-precision source coordinates: the tile origin's source position
                 // (fp64, sRot) plus an fp32 offset of at most 2 x 32 pixels
-                const float dr = (float)rr, dc = (float)tc;
+                const float dr = (float)rr, dc = (float)cc;
                 float fa = 0.f, fb = 0.f;
                 int ci = 0, ri = 0;
                 bool okr0 = false, okr1 = false, okc0 = false, okc1 = false;
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
                     v[b] = acc;
                 }
             }
-            if (job.out) {
+            if (job.out && !swp) {
 #pragma unroll
                 for (int b = 0; b < BB; ++b)
                     if (b0 + b < a.B) job.out[(b0 + b) * nn + (long)r * n + c] = v[b];
@@ -130,10 +135,24 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
         float *tp = reinterpret_cast<float *>(&t);
 #pragma unroll
         for (int b = 0; b < BB; ++b) tp[b] = v[b];
-        *reinterpret_cast<V *>(tile + rr * kRow + tc * BB) = t;
+        *reinterpret_cast<V *>(tile + rr * kRow + cc * BB) = t;
     }
-    if (!job.xr && !job.xc) return;
+    const bool late_out = swp && job.out;
+    if (!job.xr && !job.xc && !late_out) return;
     __syncthreads();
+    if (late_out) {  // plain output of a transposed-mapping tile, row by row
+        const int c = c0 + tc;
+#pragma unroll
+        for (int i = 0; i < kT / 8; ++i) {
+            const int rr = tr + 8 * i, r = r0 + rr;
+            if (r >= n || c >= n) continue;
+            const V t = *reinterpret_cast<const V *>(tile + rr * kRow + tc * BB);
+            const float *tp = reinterpret_cast<const float *>(&t);
+#pragma unroll
+            for (int b = 0; b < BB; ++b)
+                if (b0 + b < a.B) job.out[(b0 + b) * nn + (long)r * n + c] = tp[b];
+        }
+    }
     const long grp = (long)blockIdx.y * a.nblk * n * 32;  // floats per image group per class
     const int lim = a.nblk * R;                            // packed lines (incl. zero padding)
     // each item is one pixel-line slot of BB floats (16 / 8 / 4 bytes); consecutive threads
