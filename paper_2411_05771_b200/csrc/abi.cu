@@ -84,8 +84,9 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     off += align256(sizeof(float) * adj_il_floats(plan, B, m));
     w.ri = off;
     off += align256(sizeof(float) * adj_il_floats(plan, B, m));
-    w.aux = off;  // skei_sketch_deviation: the full angle list and per-image fp64 norms
-    off += align256(sizeof(int32_t) * (size_t)plan->n_full) + align256(sizeof(double) * (size_t)B);
+    w.aux = off;  // skei_sketch_deviation: the full angle list and the fp64 norm partials
+    off += align256(sizeof(int32_t) * (size_t)plan->n_full) +
+           align256(sizeof(double) * (size_t)B * kNormChunks);
     w.total = off;
     return w;
 }
@@ -420,15 +421,15 @@ skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
     int32_t *all = reinterpret_cast<int32_t *>(ws_f(ws, w.aux));
-    double *norm2 = reinterpret_cast<double *>((char *)ws + w.aux +
+    double *npart = reinterpret_cast<double *>((char *)ws + w.aux +  // norm partials
                                                align256(sizeof(int32_t) * (size_t)nf));
     float *pf = ws_f(ws, w.q), *ps = ws_f(ws, w.ri);
     float *u = ws_f(ws, w.pack[2]), *dv = ws_f(ws, w.pack[3]);
     const long per = (long)plan->n * plan->n;
     SKEI_CUDA(launch_iota(all, nf, s));
     // v <- v / ||v||
-    SKEI_CUDA(launch_sumsq(v, B, per, norm2, s));
-    SKEI_CUDA(launch_normalise(v, v, B, per, norm2, nullptr, plan->num_sms, s));
+    SKEI_CUDA(launch_sumsq(v, B, per, npart, s));
+    SKEI_CUDA(launch_normalise(v, v, B, per, npart, nullptr, plan->num_sms, s));
     const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
     for (int it = 0; it < iters; ++it) {
         RotPackJob pj{v, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
@@ -441,8 +442,8 @@ skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_
         SKEI_CUDA(launch_radon_adj(plan, &a1, 1, B, all, nf, 0, s));
         AdjJob a2{ps, dv, (float)((double)nf / m), nullptr, u};  // D v = u + (n_full/m) A_S^T A_S v
         SKEI_CUDA(launch_radon_adj(plan, &a2, 1, B, idx, m, idx_stride, s));
-        SKEI_CUDA(launch_sumsq(dv, B, per, norm2, s));
-        SKEI_CUDA(launch_normalise(dv, v, B, per, norm2, lambda, plan->num_sms, s));
+        SKEI_CUDA(launch_sumsq(dv, B, per, npart, s));
+        SKEI_CUDA(launch_normalise(dv, v, B, per, npart, lambda, plan->num_sms, s));
     }
     return SKEI_OK;
 }

@@ -131,9 +131,10 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
                              const AdjEi *ei = nullptr, int row0 = 0, int rows = -1);
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
-// Theorem-1 deviation helpers (deviation.cu)
-cudaError_t launch_sumsq(const float *w, int B, long per, double *norm2, cudaStream_t s);
-cudaError_t launch_normalise(const float *w, float *v, int B, long per, const double *norm2,
+// Theorem-1 deviation helpers (deviation.cu): part = [B][kNormChunks] fp64 chunk partials
+constexpr int kNormChunks = 128;
+cudaError_t launch_sumsq(const float *w, int B, long per, double *part, cudaStream_t s);
+cudaError_t launch_normalise(const float *w, float *v, int B, long per, const double *part,
                              float *lambda, int num_sms, cudaStream_t s);
 cudaError_t launch_iota(int32_t *a, int n, cudaStream_t s);
 // REI: pn = p + sigma eps (rei.cu; R23)
