@@ -188,36 +188,69 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
 // o whose source position (r', c') has p among its 4 bilinear neighbours, with w the
 // bilinear weight o gives p.  Those o lie in the image of the square |r' - rp| < 1,
 // |c' - cp| < 1 under the inverse rotation, whose bounding box has half-width
-// |cos g| + |sin g| <= sqrt 2: a 4 x 4 candidate window around p's inverse image.  Each
-// candidate's source position is formed in fp64 (as the oracle's definition) and the
-// weight is nonzero only if p is one of its neighbours.  One thread per pixel and 4 rows,
+// |cos g| + |sin g| <= sqrt 2: a 4 x 4 candidate window around p's inverse image.  Source
+// positions in split precision as in k_rotate_pack: a reference output pixel near the
+// tile's inverse image has its source position in fp64 (integer part + fp32 fraction), each
+// candidate adds an fp32 offset of <= ~50 px (exact at quarter turns); the weight is
+// nonzero only if p is one of the candidate's neighbours.  One thread per pixel and 4 rows,
 // the BB images of a group share the weights when g is shared.
+struct AdjRef {
+    int ro, co;      // the reference output pixel
+    int ri, ci;      // integer parts of its source position (r', c')
+    float rf, cf;    // fractional parts
+    float cg, sg;    // cos g, sin g
+    float uo0, vo0;  // inverse image of the tile origin pixel, relative to (ro, co)
+};
 template <int BB>
 __global__ void __launch_bounds__(kThreads) k_rotate_adj(const float *y, float *out, int n, int B,
                                                          const int32_t *g, int g_stride,
                                                          const double2 *rot, int tiles_c) {
+    __shared__ AdjRef sref;
     const int tc = threadIdx.x & 31, tr = threadIdx.x >> 5;
     const int r0 = blockIdx.x / tiles_c * kT, c0 = blockIdx.x % tiles_c * kT;
     const int b0 = blockIdx.y * BB;
     const long nn = (long)n * n;
-    const double h = (n - 1) * 0.5;
     const int c = c0 + tc;
     const int nimg = g_stride ? 1 : BB;  // images sharing one rotation per weight pass
 #pragma unroll 1
     for (int bs = 0; bs < BB; bs += nimg) {
         if (b0 + bs >= B) break;
-        const int gd = g[g_stride ? b0 + bs : 0];
-        const double2 csg = rot[((gd % 360) + 360) % 360];  // exact at multiples of 90
-        const double cg = csg.x, sg = csg.y;
-        const double wbox = fabs(cg) + fabs(sg);
+        if (threadIdx.x == 0) {
+            const int gd = g[g_stride ? b0 + bs : 0];
+            const double2 csg = rot[((gd % 360) + 360) % 360];  // exact at multiples of 90
+            const double cg = csg.x, sg = csg.y, h = (n - 1) * 0.5;
+            // inverse image of the tile origin pixel (r0, c0): the reference output pixel
+            const double up = c0 - h, vp = h - r0;
+            const double uo = up * cg - vp * sg, vo = up * sg + vp * cg;
+            AdjRef rf;
+            rf.co = (int)floor(uo + h);
+            rf.ro = (int)floor(h - vo);
+            // its source position (the forward definition), split
+            const double u = rf.co - h, v = h - rf.ro;
+            const double cs = u * cg + v * sg + h, rs = h - (-u * sg + v * cg);
+            const double fcs = floor(cs), frs = floor(rs);
+            rf.ci = (int)fcs;
+            rf.ri = (int)frs;
+            rf.cf = (float)(cs - fcs);
+            rf.rf = (float)(rs - frs);
+            rf.cg = (float)cg;
+            rf.sg = (float)sg;
+            rf.uo0 = (float)(uo + h - rf.co);  // column of the tile origin's inverse image
+            rf.vo0 = (float)(h - vo - rf.ro);  // row
+            sref = rf;
+        }
+        __syncthreads();
+        const AdjRef rf = sref;
+        const float wbox = fabsf(rf.cg) + fabsf(rf.sg);
 #pragma unroll 1
         for (int i = 0; i < kT / 8; ++i) {
-            const int r = r0 + tr + 8 * i;
+            const int rr = tr + 8 * i, r = r0 + rr;
             if (r >= n || c >= n) continue;
-            // inverse image of p's centre: u_o = u' cos - v' sin, v_o = u' sin + v' cos
-            const double up = c - h, vp = h - r;
-            const double uo = up * cg - vp * sg, vo = up * sg + vp * cg;
-            const int ocmin = (int)floor(uo + h - wbox), ormin = (int)floor(h - vo - wbox);
+            // p's inverse image relative to the reference: origin's + the rotated offset
+            const float dpc = (float)tc, dpr = (float)rr;
+            const float ocf = rf.uo0 + fmaf(dpc, rf.cg, dpr * rf.sg);   // d u_o / d c = cos, d u_o / d r = sin
+            const float orf = rf.vo0 + fmaf(-dpc, rf.sg, dpr * rf.cg);  // d r_o / d c = -sin, d r_o / d r = cos
+            const int ocmin = rf.co + (int)floorf(ocf - wbox), ormin = rf.ro + (int)floorf(orf - wbox);
             float acc[BB];
 #pragma unroll
             for (int b = 0; b < BB; ++b) acc[b] = 0.f;
@@ -229,15 +262,15 @@ __global__ void __launch_bounds__(kThreads) k_rotate_adj(const float *y, float *
                 for (int dc = 0; dc < 4; ++dc) {
                     const int co = ocmin + dc;
                     if (co < 0 || co >= n) continue;
-                    // source position of output pixel (ro, co), as in the forward definition
-                    const double u = co - h, v = h - ro;
-                    const double us = u * cg + v * sg, vs = -u * sg + v * cg;
-                    const double cs = us + h, rs = h - vs;
-                    const double fr = floor(rs), fc = floor(cs);
-                    const int er = r - (int)fr, ec = c - (int)fc;  // p relative to (floor r', floor c')
+                    // source position of output pixel (ro, co): reference + fp32 offset
+                    const float oc = (float)(co - rf.co), orr = (float)(ro - rf.ro);
+                    const float cl = rf.cf + fmaf(oc, rf.cg, -orr * rf.sg);
+                    const float rl = rf.rf + fmaf(oc, rf.sg, orr * rf.cg);
+                    const float flc = floorf(cl), flr = floorf(rl);
+                    const int er = r - (rf.ri + (int)flr), ec = c - (rf.ci + (int)flc);
                     if (er < 0 || er > 1 || ec < 0 || ec > 1) continue;
-                    const double a = rs - fr, bb = cs - fc;
-                    const float w = (float)((er ? a : 1.0 - a) * (ec ? bb : 1.0 - bb));
+                    const float a = rl - flr, bb = cl - flc;
+                    const float w = (er ? a : 1.f - a) * (ec ? bb : 1.f - bb);
                     const long oo = (long)ro * n + co;
 #pragma unroll
                     for (int b = 0; b < BB; ++b)
@@ -249,6 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_rotate_adj(const float *y, float *
             for (int b = 0; b < BB; ++b)
                 if (b < nimg && b0 + bs + b < B) out[(b0 + bs + b) * nn + (long)r * n + c] = acc[b];
         }
+        __syncthreads();  // sref is rewritten by the next image's pass
     }
 }
 
