@@ -41,8 +41,8 @@ __device__ __constant__ float kS16[8] = {0.0f, 0.38268343236508978f, 0.707106781
 
 // In-register DFT of size R: y_q = sum_r v_r exp(-+2 pi i q r / R) (iterative radix-2,
 // bit-reversed inputs, natural-order outputs).
-template <int R>
-__device__ __forceinline__ void dft(float2 (&v)[R], bool inverse) {
+template <int R, bool inverse>
+__device__ __forceinline__ void dft(float2 (&v)[R]) {
     constexpr int L = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -112,13 +112,14 @@ __device__ __forceinline__ float *il_row(const RampArgs &a, int row) {
     return a.qi + ((long)((b / a.bb) * a.m + k) * a.wp + kAdjPad) * a.bb + b % a.bb;
 }
 
-// One Stockham pass (in place on z): J = 16/R butterflies per thread.  mode flags:
+// One Stockham pass (in place on z): J = 16/R butterflies per thread.  Compile-time mode
+// flags (with the direction, so each pass instance carries only its own branches):
 // kIn = read the two input rows from global (first forward pass), kScale = multiply by
 // R[i] as loaded (first inverse pass), kOut = write the two output rows to global (last
 // inverse pass); otherwise smem -> smem.
 constexpr int kIn = 1, kScale = 2, kOut = 4;
-template <int R, bool PEERS>
-__device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool inverse, int mode,
+template <int R, bool PEERS, int mode, bool inverse>
+__device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip,
                                      const float *pa, const float *pb, float *qa, float *qb, float *ia, float *ib,
                                      long peer_a, long peer_b) {
     constexpr int J = 16 / R;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void pass(float2 *z, const RampArgs &a, int ip, bool 
                 v[jj][r] = inverse ? cmulc(v[jj][r], __ldg(t + (long)r * Ns))
                                    : cmul(v[jj][r], __ldg(t + (long)r * Ns));
         }
-        dft<R>(v[jj], inverse);
+        dft<R, inverse>(v[jj]);
         const int d = (j - k) * R + k;
         if (mode & kOut) {
 #pragma unroll
@@ -232,15 +233,22 @@ __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
     float *ib = a.qi && has_b ? il_row(a, rb) : nullptr;
     const long pa_off = PEERS ? peer_off(ra) : 0, pb_off = PEERS && has_b ? peer_off(rb) : 0;
     const int last = a.npass - 1;
-    // forward: radix-16 passes then the RL pass
-    for (int ip = 0; ip < last; ++ip)
-        pass<16, PEERS>(z, a, ip, false, ip == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
-    pass<RL, PEERS>(z, a, last, false, last == 0 ? kIn : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
-    // inverse of R . FFT(z)
-    for (int ip = 0; ip < last; ++ip)
-        pass<16, PEERS>(z, a, ip, true, ip == 0 ? kScale : 0, pa, pb, qa, qb, ia, ib, pa_off, pb_off);
-    pass<RL, PEERS>(z, a, last, true, kOut | (last == 0 ? kScale : 0), pa, pb, qa, qb, ia, ib,
-                    pa_off, pb_off);
+#define SKEI_PASS(RV, MODE, INV, IP) \
+    pass<RV, PEERS, MODE, INV>(z, a, IP, pa, pb, qa, qb, ia, ib, pa_off, pb_off)
+    if (last == 0) {  // a single pass each way (P <= 16)
+        SKEI_PASS(RL, kIn, false, 0);
+        SKEI_PASS(RL, kOut | kScale, true, 0);
+    } else {
+        // forward: radix-16 passes (the first reads the rows from global) then the RL pass
+        SKEI_PASS(16, kIn, false, 0);
+        for (int ip = 1; ip < last; ++ip) SKEI_PASS(16, 0, false, ip);
+        SKEI_PASS(RL, 0, false, last);
+        // inverse of R . FFT(z): the first pass scales by R[k], the last writes the rows
+        SKEI_PASS(16, kScale, true, 0);
+        for (int ip = 1; ip < last; ++ip) SKEI_PASS(16, 0, true, ip);
+        SKEI_PASS(RL, kOut, true, last);
+    }
+#undef SKEI_PASS
     if (ia) {  // the zero pads of the interleaved rows
         for (int t = threadIdx.x; t < 2 * kAdjPad; t += blockDim.x) {
             const int o = t < kAdjPad ? t - kAdjPad : a.n_det + (t - kAdjPad);
