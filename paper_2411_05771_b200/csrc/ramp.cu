@@ -16,8 +16,9 @@
 // every pass); the first pass reads the rows straight from global memory, the spectrum is
 // multiplied by R[k]/P as the inverse transform loads it, and the last inverse pass writes
 // the two output rows straight to global memory.  Twiddles w^(rk) come from per-pass plan
-// tables computed in fp64 and rounded once (no recurrences, no fast intrinsics); the
-// in-register DFT uses the exact 16th roots of unity as literals.
+// tables computed in fp64 and rounded once (no recurrences, no fast intrinsics), stored
+// r-major so a warp's loads are coalesced; the in-register DFT uses the exact 16th roots of
+// unity as literals.  Each pass's mode and direction are template parameters.
 #include "internal.h"
 
 namespace skei {

@@ -13,7 +13,11 @@
 // i.e. the image cut into blocks of R lines, each block stored pixel-major with the R lines
 // x BB images of one pixel in 128 contiguous bytes — the layout k_radon_fwd stages with one
 // TMA bulk copy per block.  Pixels outside the image (the last block's
-// padding lines) are written as zeros.  The identity job (g = 0, no taps) packs x1.
+// padding lines) are written as zeros.  The identity job (g = 0, no taps) packs x1.  With a
+// shared g the BB images share one set of taps per pixel; for |sin g| > |cos g| a warp's
+// lanes take 32 rows of one column (taps stay within a few cache lines).  Behind the pass's
+// own draw kernel (skei_pass_draw) the launch is programmatically serialised: only the
+// rotation job waits (griddepcontrol.wait) for g.
 #include "internal.h"
 
 namespace skei {
