@@ -39,7 +39,7 @@
 //     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
 //   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset (split precision,
 //     DESIGN.md §5), 3 hat weights, 3 LDS.BB (the third skipped when its weight is 0) issued
-//     kAhead = 2 lines ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
+//     kAhead = 1 line ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
 //     summed into a partial before it is added to the running total (two-level summation).
 //     A chunk skips a block none of its 32 bins sees.
 //   * Unit end: a whole unit's sums are complete in registers -> p; for the MC job also
@@ -58,11 +58,14 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
 // 32-bin task slots per warp (each lane: kMaxT * BB accumulator registers)
+#ifndef SKEI_FWD_KT4
+#define SKEI_FWD_KT4 8
+#endif
 template <int BB>
-constexpr int max_tasks() { return 8; }
+constexpr int max_tasks() { return BB == 4 ? SKEI_FWD_KT4 : 8; }
 constexpr int kKMax = 16;   // angles per CTA
 #ifndef SKEI_FWD_AHEAD
-#define SKEI_FWD_AHEAD 2
+#define SKEI_FWD_AHEAD 1
 #endif
 constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ahead of use
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
@@ -751,7 +754,8 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
 size_t fwd_scratch_floats(const skei_plan *plan) {
     // two split-unit piece slots per CTA (grid <= num_sms), each K * n_det * BB <=
     // kWarps * kMaxT * 32 * 4 floats
-    return (size_t)2 * plan->num_sms * kWarps * max_tasks<1>() * 32 * 4;
+    constexpr int kt = max_tasks<4>() > max_tasks<1>() ? max_tasks<4>() : max_tasks<1>();
+    return (size_t)2 * plan->num_sms * kWarps * kt * 32 * 4;
 }
 
 size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
