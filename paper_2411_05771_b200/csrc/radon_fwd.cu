@@ -57,20 +57,28 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
-// 32-bin task slots per warp (each lane: kMaxT * BB accumulator registers)
+constexpr int kChunk = 64;  // bins per task: lane L owns the pair c0 + 2L, c0 + 2L + 1
+// task slots per warp (each lane: kMaxT * 2 * BB accumulator registers)
 #ifndef SKEI_FWD_KT4
-#define SKEI_FWD_KT4 8
+#define SKEI_FWD_KT4 4
 #endif
 template <int BB>
-constexpr int max_tasks() { return BB == 4 ? SKEI_FWD_KT4 : 8; }
+constexpr int max_tasks() { return BB == 4 ? SKEI_FWD_KT4 : BB == 2 ? 8 : 8; }
+// max over BB of kMaxT * BB (a split unit's piece: K * n_det * BB <= kWarps * kMaxT * kChunk * BB
+// floats) and min over BB of kMaxT (the most units an image group can have)
+constexpr int cmax_(int a, int b) { return a > b ? a : b; }
+constexpr int kMaxTaskBB = cmax_(cmax_(4 * max_tasks<4>(), 2 * max_tasks<2>()), max_tasks<1>());
+constexpr int kMinTasks = max_tasks<4>() < max_tasks<2>() ? max_tasks<4>() : max_tasks<2>();
+static_assert(kMinTasks <= max_tasks<1>(), "");
 constexpr int kKMax = 16;   // angles per CTA
 #ifndef SKEI_FWD_AHEAD
 #define SKEI_FWD_AHEAD 1
 #endif
 constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ahead of use
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
-constexpr int kPadL = 4;    // zero pixel columns left of the line data
-constexpr int kPadR = 4;    // ... and right of it (candidates reach n + 2)
+constexpr int kCand = 5;    // candidate pixels of a bin pair per line
+constexpr int kPadL = 5;    // zero pixel columns left of the line data (candidates from -5)
+constexpr int kPadR = 5;    // ... and right of it (candidates reach n + 4)
 constexpr int kColF = 32;   // floats per staged pixel column (R * BB)
 
 struct FwdArgs {
@@ -204,7 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
     __shared__ float sAbsB[kKMax];
-    __shared__ float4 sAng[kKMax];  // |beta|, 1/|beta|, Pl, 2 - 3|beta| (fp32)
+    __shared__ float4 sAng[kKMax];   // |beta|, 1/|beta|, Pl, min(Pj, 0) (fp32)
+    __shared__ float4 sAng2[kKMax];  // 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2 (hat offsets)
     __shared__ int sSlot[kKMax];
     __shared__ int sCount;
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
@@ -323,15 +332,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     constexpr int LB = R == 32 ? 5 : R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const int lane_r = lane & (R - 1);
     const float lf0 = (float)lane_r;
-    const float lanef = (float)lane;
+    const float lane2f = (float)(2 * lane - 31);  // the lane's pair relative to the chunk's middle
     float sgn[LB];  // +-2^i: + if bit i of lane' is 0 (flipping it on moves the line up)
 #pragma unroll
     for (int i = 0; i < LB; ++i) sgn[i] = ((lane_r >> i) & 1) ? -(float)(1 << i) : (float)(1 << i);
-    // byte offset of line lane' in a staged pixel column, plus the pad shift (3 pad columns,
-    // see the clamp below); bits 0..6, the buffer bases are 128-byte aligned
-    const unsigned lofs0 = (unsigned)(((kPadL - 3) * kColF + lane_r * BB) * sizeof(float));
+    // byte offset of line lane' in a staged pixel column (the clamp below addresses pixel
+    // columns from the first pad column, kPadL = kCand); bits 0..6, the buffer bases are
+    // 128-byte aligned
+    static_assert(kPadL == kCand && kPadR >= kCand, "pads must hold a whole candidate window");
+    const unsigned lofs0 = (unsigned)(lane_r * BB * sizeof(float));
     const unsigned smem_b = smem_u32(smem);
-    const unsigned cmax = (unsigned)(n + 3);
+    const unsigned cmax = (unsigned)(n + kCand);
 
 #ifdef SKEI_FWD_STATS
     long long st_wait = 0, st_epi = 0, st_pro = 0, st_active = 0, st_lanes = 0;
@@ -390,7 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 sPl[lane] = Pl;
                 sAbsB[lane] = (float)ab;
                 sAng[lane] = make_float4((float)ab, (float)(1.0 / ab), (float)Pl,
-                                         (float)(2.0 - 3.0 * ab));
+                                         (float)fmin(Pj, 0.0));
+                sAng2[lane] = make_float4((float)(2.0 * ab - 1.0), (float)(3.0 * ab - 2.0),
+                                          (float)(4.0 * ab - 2.0), (float)(5.0 * ab - 2.0));
             }
         }
         for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads) s_cost[tau] = 0;
@@ -416,20 +429,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             ent.z = (int)jl;
             ent.w = (int)jh;
             btab[e] = ent;
-            // the chunks c with 32 c <= jh and 32 c + 31 >= jl touch this block
-            const int clo = ent.z <= 0 ? 0 : ent.z / 32;
-            const int chi = ent.w < 0 ? -1 : min(a.chunks - 1, ent.w / 32);
+            // the chunks c with 64 c <= jh and 64 c + 63 >= jl touch this block
+            const int clo = ent.z <= 0 ? 0 : ent.z / kChunk;
+            const int chi = ent.w < 0 ? -1 : min(a.chunks - 1, ent.w / kChunk);
             for (int c = clo; c <= chi; ++c) atomicAdd(&s_cost[k * a.chunks + c], 1);
         }
 
-        // ---- 3. tasks: (angle k, 32-bin chunk) pairs.  A warp runs a task's whole line loop
+        // ---- 3. tasks: (angle k, 64-bin chunk) pairs.  A warp runs a task's whole line loop
         // on every block its chunk touches, so a task costs the number of such blocks
         // (counted while the block table is built); chunks that touch no block are dropped.
         // The others are ranked by cost (descending, ties by index) and dealt to the warps
         // in snake order (rank r -> round r / kWarps, warp r mod kWarps, reversed on odd
         // rounds), which balances the warps to within about one task.  Per task: angle slot
-        // k (< 0: none), first bin of the chunk c0, and c0 Pj split into (int, fp32
-        // fraction) in fp64; a lane adds its lane Pj in fp32.
+        // k (< 0: none), first bin of the chunk c0, and (c0 + 31) Pj + min(Pj, 0) split into
+        // (int, fp32 fraction) in fp64; a lane adds its (2 lane - 31) Pj in fp32 (|.| < 44),
+        // giving the position of the lower of its two bins (the one nearer pixel 0).
         __syncthreads();  // block table and task costs complete
         for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads)
             s_task[tau] = make_int4(-1, 0, 0, 0);
@@ -446,8 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             const int w = (round & 1) ? kWarps - 1 - wi : wi;
             int4 td;
             td.x = tau / a.chunks;
-            td.y = (tau - td.x * a.chunks) * 32;
-            const double J = (double)td.y * sPj[td.x];
+            td.y = (tau - td.x * a.chunks) * kChunk;
+            const double J = (double)(td.y + 31) * sPj[td.x] + fmin(sPj[td.x], 0.0);
             const double fJ = floor(J);
             td.z = (int)fJ;
             td.w = __float_as_int((float)(J - fJ));
@@ -457,11 +471,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #ifdef SKEI_FWD_STATS
         st_pro += clock64() - tp0;
 #endif
-        float acc[kMaxT][BB];
+        // acc[t][0..BB): the lower bin of the lane's pair (the one nearer pixel 0 of the
+        // line), acc[t][BB..2BB): the upper one
+        float acc[kMaxT][2 * BB];
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t)
 #pragma unroll
-            for (int b = 0; b < BB; ++b) acc[t][b] = 0.f;
+            for (int b = 0; b < 2 * BB; ++b) acc[t][b] = 0.f;
 
         for (int i = 0; i < nbu; ++i) {
             const int g = gbase + i;
@@ -475,17 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             st_wait += clock64() - tw0;
 #endif
             int4 tdn = s_task[warp];  // the next task's descriptor, loaded one task ahead
-#pragma unroll
+            // the task loop is unrolled (acc[t] register-indexed) only while the code stays
+            // small; otherwise each task's block sum is added to acc[t] by predicated adds
+            constexpr bool kUnrollT = R * kMaxT <= 64;
+#pragma unroll(kUnrollT ? kMaxT : 1)
             for (int t = 0; t < kMaxT; ++t) {
                 const int4 td = tdn;  // warp-uniform (broadcast)
                 const int k = td.x;
                 if (k < 0) break;
                 const int4 ent = btab[k * nbu + i];
                 if (t + 1 < kMaxT) tdn = s_task[warp + kWarps * (t + 1)];
-                if (td.y > ent.w || td.y + 31 < ent.z) continue;  // chunk misses the block
+                if (td.y > ent.w || td.y + kChunk - 1 < ent.z) continue;  // chunk misses the block
 #ifdef SKEI_FWD_STATS
                 ++st_active;
-                st_lanes += max(0, min(td.y + 31, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
+                st_lanes += max(0, min(td.y + kChunk - 1, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
 #endif
                 int base = ent.x + td.z;
                 float frac = __int_as_float(ent.y) + __int_as_float(td.w);
@@ -493,44 +512,76 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     frac -= 1.f;
                     base += 1;
                 }
-                const float4 ang = sAng[k];  // |beta|, 1/|beta|, Pl, 2 - 3|beta|
-                const float ab = ang.x, plf = ang.z, c2 = ang.w;
-                const float c1 = fmaf(2.f, ab, -1.f);
-                // + lane Pj (< 32 * sqrt 2, fp32): the lane's bin within the chunk
-                const float fs = fmaf(lanef, sPjf[k], frac - ang.y);
-                // candidate_0 + 3 = base + 4 + floor(e); floor(e) is taken as an exact fp32
-                // integer and moved to the integer unit by the 1.5 * 2^23 bias (|e| < 2^22)
-                const int base4 = base + 4 - 0x4B400000;
+                const float4 ang = sAng[k];   // |beta|, 1/|beta|, Pl, min(Pj, 0)
+                const float4 off = sAng2[k];  // hat offsets 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2
+                const float ab = ang.x, plf = ang.z;
+                // a candidate window of 5 pixels can be needed only if 4|beta| - 1 < 2
+                const bool wide = off.z < 1.f;
+                // + (2 lane - 31) Pj (|.| < 44, fp32): the lane's lower bin within the chunk
+                const float fs = fmaf(lane2f, sPjf[k], frac - ang.y);
+                // candidate_0 + kCand = base + 6 + floor(e); floor(e) is taken as an exact
+                // fp32 integer and moved to the integer unit by the 1.5 * 2^23 bias (|e| < 2^22)
+                const int base6 = base + 1 + kCand - 0x4B400000;
                 float d[LB];
 #pragma unroll
                 for (int b = 0; b < LB; ++b) d[b] = sgn[b] * plf;
-                const unsigned pbase = cur_b + lofs0;  // bits 0..6 = line lane' (+ pad shift)
+                const unsigned pbase = cur_b + lofs0;  // bits 0..6 = line lane'
                 float e = fmaf(lf0, plf, fs);
-                float blk[BB];
+                float lo[BB], hi[BB];
 #pragma unroll
-                for (int b = 0; b < BB; ++b) blk[b] = 0.f;
-                // one line: e = a* - 1/|beta| relative to base; candidate_0 = floor(e) + 1 and
-                // with phi = e - floor(e) the hat weights of the 3 candidates are
-                //   w0 = |b| (1 - phi), w1 = 1 - |2|b| - 1 - |b| phi|, w2 = 2 - 3|b| + |b| phi;
-                // the 2-3 candidate pixels are loaded kAhead lines ahead of their use
+                for (int b = 0; b < BB; ++b) lo[b] = hi[b] = 0.f;
+                // one line: e = a*_lo - 1/|beta| relative to base (a*_lo: the line position
+                // that projects onto the lower bin's centre, the upper one's is a*_lo + 1/|b|).
+                // Candidates c_k = floor(e) + 1 + k, k = 0..4, lie at detector offsets
+                // delta_k = |b| (k + 1 - phi) - 1 from the lower bin (phi = e - floor(e)), so
+                // their hat weights are, for the lower bin,
+                //   w0 = |b| (1 - phi), w1 = 1 - |d1|, w2 = max(0, -(d2 - 1))
+                // and for the upper bin (hat(delta - 1))
+                //   w1' = max(0, d1), w2' = 1 - |d2 - 1|, w3' = max(0, 1 - (d3 - 1)),
+                //   w4' = max(0, 1 - (d4 - 1)),
+                // every other (candidate, bin) weight being 0 for |beta| in [1/sqrt 2, 1].
+                // The 5 candidate pixels are loaded kAhead lines ahead of their use; c3 only
+                // where w3' > 0, c4 only where w4' > 0 (possible only if 4|b| - 1 < 2).
                 constexpr int D = kAhead < R ? kAhead : R - 1;  // lines in flight ahead of use
-                float v[D + 1][3][BB], w[D + 1][3];
-                auto load_line = [&](int st, float (&vv)[3][BB], float (&ww)[3]) {
+                float v[D + 1][kCand][BB], ph[D + 1];
+                auto load_line = [&](int st, float (&vv)[kCand][BB], float &phs) {
                     const int gc = st ^ (st >> 1);
                     const float fl2 = floorf(e);
                     const float phi = e - fl2;
-                    // candidate_0 + 3 clamped to [0, n + 3] in one unsigned min (lanes whose
-                    // bin misses the line land in the zero pad columns)
+                    phs = phi;
+                    // candidate_0 + 5 clamped to [0, n + 5] in one unsigned min (lanes whose
+                    // pair misses the line land in the zero pad columns)
                     const unsigned cu =
-                        min((unsigned)(base4 + __float_as_int(fl2 + 12582912.f)), cmax);
-                    ww[0] = fmaf(-ab, phi, ab);
-                    ww[1] = 1.f - fabsf(fmaf(-ab, phi, c1));
-                    ww[2] = fmaf(ab, phi, c2);
+                        min((unsigned)(base6 + __float_as_int(fl2 + 12582912.f)), cmax);
                     const unsigned pa = (pbase ^ (unsigned)(gc * BB * sizeof(float))) +
                                         cu * (unsigned)(kColF * sizeof(float));
                     lds_px<BB>(pa, vv[0]);
                     lds_px<BB>(pa + kColF * sizeof(float), vv[1]);
-                    if (ww[2] > 0.f) lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
+                    lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
+                    if (fmaf(-ab, phi, off.z) < 1.f) lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
+                    if (wide) {
+                        if (fmaf(-ab, phi, off.w) < 1.f)
+                            lds_px<BB>(pa + 4 * kColF * sizeof(float), vv[4]);
+                    }
+                };
+                auto use_line = [&](const float (&vv)[kCand][BB], float phi) {
+                    const float w0 = fmaf(-ab, phi, ab);
+                    const float d1 = fmaf(-ab, phi, off.x);
+                    const float e2 = fmaf(-ab, phi, off.y);
+                    const float e3 = fmaf(-ab, phi, off.z);
+                    const float w1 = 1.f - fabsf(d1), u1 = fmaxf(d1, 0.f);
+                    const float w2 = fmaxf(-e2, 0.f), u2 = 1.f - fabsf(e2);
+                    const float u3 = fmaxf(1.f - e3, 0.f);
+                    fma_px<BB>(lo, w0, vv[0]);
+                    fma_px<BB>(lo, w1, vv[1]);
+                    fma_px<BB>(hi, u1, vv[1]);
+                    fma_px<BB>(lo, w2, vv[2]);
+                    fma_px<BB>(hi, u2, vv[2]);
+                    fma_px<BB>(hi, u3, vv[3]);
+                    if (wide) {
+                        const float u4 = fmaxf(1.f - fmaf(-ab, phi, off.w), 0.f);
+                        fma_px<BB>(hi, u4, vv[4]);
+                    }
                 };
                 // e of line gray(sn) from that of line gray(sn - 1)
                 auto advance = [&](int sn) {
@@ -543,24 +594,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                         e = ((gc >> ib) & 1) ? e + d[ib] : e - d[ib];
                     }
                 };
+                // c3 / c4 are not loaded where their weight is 0: keep their registers finite
+#pragma unroll
+                for (int q2 = 0; q2 <= D; ++q2)
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) v[q2][3][b] = v[q2][4][b] = 0.f;
 #pragma unroll
                 for (int st = 0; st < D; ++st) {
                     if (st > 0) advance(st);
-                    load_line(st, v[st], w[st]);
+                    load_line(st, v[st], ph[st]);
                 }
 #pragma unroll
                 for (int st = 0; st < R; ++st) {
                     const int cur = st % (D + 1);
                     if (st + D < R) {
                         advance(st + D);
-                        load_line(st + D, v[(st + D) % (D + 1)], w[(st + D) % (D + 1)]);
+                        load_line(st + D, v[(st + D) % (D + 1)], ph[(st + D) % (D + 1)]);
                     }
-                    fma_px<BB>(blk, w[cur][0], v[cur][0]);
-                    fma_px<BB>(blk, w[cur][1], v[cur][1]);
-                    if (w[cur][2] > 0.f) fma_px<BB>(blk, w[cur][2], v[cur][2]);
+                    use_line(v[cur], ph[cur]);
                 }
+                if constexpr (kUnrollT) {
 #pragma unroll
-                for (int b = 0; b < BB; ++b) acc[t][b] += blk[b];
+                    for (int b = 0; b < BB; ++b) {
+                        acc[t][b] += lo[b];
+                        acc[t][BB + b] += hi[b];
+                    }
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < kMaxT; ++tt)
+                        if (tt == t) {
+#pragma unroll
+                            for (int b = 0; b < BB; ++b) {
+                                acc[tt][b] += lo[b];
+                                acc[tt][BB + b] += hi[b];
+                            }
+                        }
+                }
             }
             // release the buffer; the last warp out refills it with block g + nbuf
             __syncwarp();
@@ -588,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         float racc[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) racc[b] = 0.f;
-        auto finish_pair = [&](int slot, int j, const float (&sv)[BB]) {
+        auto finish_bin = [&](int slot, int j, const float (&sv)[BB]) {
             const long pj = (long)slot * n_det + j;
 #pragma unroll
             for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
@@ -608,18 +677,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         float zero[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) zero[b] = 0.f;
+        // the lane's pair (j0, j0 + 1) of task t: acc holds (lower, upper); the lower bin is
+        // j0 unless Pj < 0
+        auto pair_sums = [&](int t, float (&s0)[BB], float (&s1)[BB]) {
+            const bool neg = sAng[s_task[warp + kWarps * t].x].w < 0.f;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                s0[b] = neg ? acc[t][BB + b] : acc[t][b];
+                s1[b] = neg ? acc[t][b] : acc[t][BB + b];
+            }
+        };
         if (full_unit) {
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
                 const int4 td = s_task[warp + kWarps * t];
                 if (td.x < 0) break;
-                const int j = td.y + lane;
-                if (j < n_det) finish_pair(sSlot[td.x], j, acc[t]);
+                const int j = td.y + 2 * lane;
+                float s0[BB], s1[BB];
+                pair_sums(t, s0, s1);
+                if (j < n_det) finish_bin(sSlot[td.x], j, s0);
+                if (j + 1 < n_det) finish_bin(sSlot[td.x], j + 1, s1);
             }
             for (int tau = warp; tau < ntask; tau += kWarps) {
                 if (s_cost[tau] != 0) continue;
-                const int k = tau / a.chunks, j = (tau - k * a.chunks) * 32 + lane;
-                if (j < n_det) finish_pair(sSlot[k], j, zero);
+                const int k = tau / a.chunks, j = (tau - k * a.chunks) * kChunk + 2 * lane;
+                if (j < n_det) finish_bin(sSlot[k], j, zero);
+                if (j + 1 < n_det) finish_bin(sSlot[k], j + 1, zero);
             }
         } else {
             float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
@@ -627,13 +710,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             for (int t = 0; t < kMaxT; ++t) {
                 const int4 td = s_task[warp + kWarps * t];
                 if (td.x < 0) break;
-                const int j = td.y + lane;
-                if (j < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j) * BB, acc[t]);
+                const int j = td.y + 2 * lane;
+                float s0[BB], s1[BB];
+                pair_sums(t, s0, s1);
+                if (j < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j) * BB, s0);
+                if (j + 1 < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j + 1) * BB, s1);
             }
             for (int tau = warp; tau < ntask; tau += kWarps) {
                 if (s_cost[tau] != 0) continue;
-                const int k = tau / a.chunks, j = (tau - k * a.chunks) * 32 + lane;
+                const int k = tau / a.chunks, j = (tau - k * a.chunks) * kChunk + 2 * lane;
                 if (j < n_det) stg_vec<BB>(mine + ((long)k * n_det + j) * BB, zero);
+                if (j + 1 < n_det) stg_vec<BB>(mine + ((long)k * n_det + j + 1) * BB, zero);
             }
             __threadfence();
             __syncthreads();  // the whole piece written (and fenced)
@@ -666,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #pragma unroll
                         for (int b = 0; b < BB; ++b) sv[b] += v[b];
                     }
-                    finish_pair(sSlot[k], o2 - k * n_det, sv);
+                    finish_bin(sSlot[k], o2 - k * n_det, sv);
                 }
             }
         }
@@ -721,7 +808,7 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     constexpr int R = kColF / BB;
     a.K = (kWarps * max_tasks<BB>()) / a.chunks;
     if (a.K > kKMax) a.K = kKMax;
-    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * 32
+    if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * kChunk
     a.nblk = (a.g.n + R - 1) / R;
     a.nq = a.B / BB;
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
@@ -734,13 +821,15 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared memory)
+    // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared memory;
+    // the split-unit scratch, the piece counters and kMaxPieces assume grid <= num_sms <= 256)
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB>, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    if (num_sms > kMaxPieces || num_sms > kPassCounters - 2) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(num_sms * per_sm), 1, 1);
+    cfg.gridDim = dim3((unsigned)num_sms, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -752,17 +841,16 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
 }  // namespace
 
 size_t fwd_scratch_floats(const skei_plan *plan) {
-    // two split-unit piece slots per CTA (grid <= num_sms), each K * n_det * BB <=
-    // kWarps * kMaxT * 32 * 4 floats
-    constexpr int kt = max_tasks<4>() > max_tasks<1>() ? max_tasks<4>() : max_tasks<1>();
-    return (size_t)2 * plan->num_sms * kWarps * kt * 32 * 4;
+    // two split-unit piece slots per CTA (grid = num_sms), each K * n_det * BB <=
+    // kWarps * kMaxT * kChunk * BB floats
+    return (size_t)2 * plan->num_sms * kWarps * kMaxTaskBB * kChunk;
 }
 
 size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
     (void)B;
     (void)idx_stride;
-    const int chunks = (plan->n_det + 31) / 32;
-    int K = (kWarps * max_tasks<1>()) / chunks;  // the smallest K over the image groups
+    const int chunks = (plan->n_det + kChunk - 1) / kChunk;
+    int K = (kWarps * kMinTasks) / chunks;  // the smallest K over the group sizes BB
     if (K > kKMax) K = kKMax;
     if (K < 1) K = 1;
     return (size_t)((m + K - 1) / K + 2);  // units per image group
@@ -786,7 +874,7 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.idx_stride = idx_stride;
     a.B = B;
     a.g = geom_of(plan);
-    a.chunks = (plan->n_det + 31) / 32;
+    a.chunks = (plan->n_det + kChunk - 1) / kChunk;
     if (!mc) a.job[0].y = nullptr;
     const int bb = fwd_bb(B, idx_stride);
     switch (bb) {
