@@ -54,7 +54,10 @@
 namespace skei {
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef SKEI_FWD_THREADS
+#define SKEI_FWD_THREADS 512
+#endif
+constexpr int kThreads = SKEI_FWD_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxQ = 1024; // image groups per launch (shared-memory unit table)
 constexpr int kChunk = 64;  // bins per task: lane L owns the pair c0 + 2L, c0 + 2L + 1
@@ -219,11 +222,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
     __shared__ float s_red[kWarps][BB];
     __shared__ bool s_last;
-    __shared__ int s_fin;       // split unit: this CTA sums the pieces (0/1)
     __shared__ int4 s_task[kWarps * kMaxT];  // per task: angle slot, chunk bin, chunk Pj split
-    __shared__ int s_piece[kMaxPieces];      // split unit: piece slot offsets in CTA order
     __shared__ int s_cost[kWarps * kMaxT];   // per task: blocks its chunk touches
-    __shared__ int s_npc;
+    __shared__ int s_defer[2], s_dnpc[2];  // split units this CTA finishes after its stream
+    __shared__ int s_dpiece[2][kMaxPieces];  // ... their piece slots in CTA order
     __shared__ float sPjf[kKMax];            // Pj (fp32)
 
     const int cid = blockIdx.x, ncl = gridDim.x;
@@ -262,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         mbar_init(&full[1], 1);
         mbar_init(&full[2], 1);
         done[0] = done[1] = done[2] = 0;
+        s_defer[0] = s_defer[1] = -1;
         fence_mbar_init();
     }
     __syncthreads();
@@ -726,34 +729,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             __syncthreads();  // the whole piece written (and fenced)
             if (threadIdx.x == 0) {
                 // the pieces: non-empty CTA ranges c0 .. c1, slot 0 if u is the CTA's first unit
+                // (the last piece to arrive finishes the unit after this CTA's block stream,
+                // step 4b, where the projector's registers are free for batched loads)
                 const int c0 = cta_of((long)u * nbc), c1 = cta_of((long)u * nbc + nbc - 1);
+                const int di = u == u_first ? 0 : 1;
                 int npc = 0;
                 for (int c = c0; c <= c1; ++c) {
                     const long ws = wstart(c);
                     if (wstart(c + 1) == ws) continue;
-                    s_piece[npc++] = c * 2 + (u == (int)(ws / nbc) ? 0 : 1);
+                    s_dpiece[di][npc++] = c * 2 + (u == (int)(ws / nbc) ? 0 : 1);
                 }
-                s_npc = npc;
                 const bool last = atomicAdd(a.queue + c0, 1u) == (unsigned)(npc - 1);
-                if (last) a.queue[c0] = 0u;  // ready for the next launch
-                s_fin = last ? 1 : 0;
-            }
-            __syncthreads();
-            finish = s_fin != 0;
-            if (finish) {
-                __threadfence();
-                const int npc = s_npc;
-                for (int o2 = threadIdx.x; o2 < kcnt * n_det; o2 += kThreads) {
-                    const int k = o2 / n_det;
-                    float sv[BB];
-                    ldcg_vec<BB>(pieces + (long)s_piece[0] * part_f + (long)o2 * BB, sv);
-                    for (int c = 1; c < npc; ++c) {  // the pieces in CTA order
-                        float v[BB];
-                        ldcg_vec<BB>(pieces + (long)s_piece[c] * part_f + (long)o2 * BB, v);
-#pragma unroll
-                        for (int b = 0; b < BB; ++b) sv[b] += v[b];
-                    }
-                    finish_bin(sSlot[k], o2 - k * n_det, sv);
+                if (last) {
+                    a.queue[c0] = 0u;  // ready for the next launch
+                    s_defer[di] = u;
+                    s_dnpc[di] = npc;
                 }
             }
         }
@@ -777,11 +767,117 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #endif
     }
 
+    // ---- 4b. split units whose last piece this CTA produced: out = the pieces summed in CTA
+    // order (p; for the MC job r = p - y_S and the unit's partial of sum r^2).  kFin outputs
+    // per thread and round, their piece and y_S loads in flight together.
+#ifdef SKEI_FWD_STATS
+    const long long tf0 = clock64();
+#endif
+    for (int di = 0; di < 2; ++di) {
+        const int u = s_defer[di];
+        if (u < 0) continue;
+        const UnitId d = decode_unit(U, nq, K, u);
+        const FwdJob job = d.job ? a.job[1] : a.job[0];
+        const int b0 = d.q * BB;
+        const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
+        __syncthreads();  // sSlot free
+        if (warp == 0) {  // the unit's angle slots, as in step 2
+            int seen = 0;
+            for (int base = 0; base < a.m; base += 32) {
+                const int k = base + lane;
+                bool in = false;
+                if (k < a.m) {
+                    const int i = idx[k];
+                    const bool row_class = (4 * i <= n_full) || (4 * i >= 3 * n_full);
+                    in = (d.cls == 0) ? row_class : !row_class;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                const int pre = seen + __popc(bal & ((1u << lane) - 1u));
+                if (in && pre >= d.grp * K && pre < d.grp * K + K) sSlot[pre - d.grp * K] = k;
+                seen += __popc(bal);
+            }
+            if (lane == 0) sCount = max(0, min(K, seen - d.grp * K));
+        }
+        __syncthreads();
+        const int total = sCount * n_det, npc = s_dnpc[di];
+        const long img_stride = (long)a.m * n_det;
+        const long ys = (long)(job.y_sketched ? a.m : n_full) * n_det;
+        const bool mc = job.y != nullptr;
+        const int *pc = s_dpiece[di];
+        float racc[BB];
+#pragma unroll
+        for (int b = 0; b < BB; ++b) racc[b] = 0.f;
+        constexpr int kFin = 4;
+        for (int o0 = threadIdx.x; o0 < total; o0 += kThreads * kFin) {
+            float sv[kFin][BB], yv[kFin][BB];
+#pragma unroll
+            for (int q = 0; q < kFin; ++q) {
+                const int o2 = o0 + q * kThreads;
+                if (o2 < total) {
+                    const int k = o2 / n_det, j = o2 - k * n_det;
+                    ldcg_vec<BB>(pieces + (long)pc[0] * part_f + (long)o2 * BB, sv[q]);
+                    if (mc) {
+                        const int slot = sSlot[k];
+                        const long yj = (long)(job.y_sketched ? slot : idx[slot]) * n_det + j;
+#pragma unroll
+                        for (int b = 0; b < BB; ++b) yv[q][b] = __ldg(job.y + (long)(b0 + b) * ys + yj);
+                    }
+                }
+            }
+            for (int c = 1; c < npc; ++c) {  // the pieces in CTA order
+                float v[kFin][BB];
+#pragma unroll
+                for (int q = 0; q < kFin; ++q)
+                    if (o0 + q * kThreads < total)
+                        ldcg_vec<BB>(pieces + (long)pc[c] * part_f + (long)(o0 + q * kThreads) * BB, v[q]);
+#pragma unroll
+                for (int q = 0; q < kFin; ++q)
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) sv[q][b] += v[q][b];
+            }
+#pragma unroll
+            for (int q = 0; q < kFin; ++q) {
+                const int o2 = o0 + q * kThreads;
+                if (o2 >= total) continue;
+                const int k = o2 / n_det, j = o2 - k * n_det;
+                const long pj = (long)sSlot[k] * n_det + j;
+#pragma unroll
+                for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[q][b];
+                if (mc) {
+#pragma unroll
+                    for (int b = 0; b < BB; ++b) {
+                        const float dr = sv[q][b] - yv[q][b];
+                        if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
+                        racc[b] = fmaf(dr, dr, racc[b]);
+                    }
+                }
+            }
+        }
+        if (mc) {  // the unit's partial of each image of the group
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                float v = racc[b];
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0) s_red[warp][b] = v;
+            }
+            __syncthreads();
+            if (threadIdx.x < BB) {
+                float v = 0.f;
+                for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
+                a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
+            }
+        }
+    }
+#ifdef SKEI_FWD_STATS
+    const long long st_fin = clock64() - tf0;
+#endif
+
 #ifdef SKEI_FWD_STATS
     if (lane == 0 && (blockIdx.x % 37) == 0)
         printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld active %lld "
-               "lanes %lld\n", blockIdx.x, warp, u_last - u_first + 1, G, st_wait, st_pro, st_epi,
-               clock64() - st_t0, st_active, st_lanes);
+               "lanes %lld esync %lld fin %lld\n", blockIdx.x, warp, u_last - u_first + 1, G, st_wait,
+               st_pro, st_epi, clock64() - st_t0, st_active, st_lanes, 0LL, st_fin);
 #endif
     // ---- 5. MC residual final: the last CTA sums each image's (unit, rank) partials in order
     if (!a.job[0].y) return;

@@ -20,7 +20,7 @@ def main():
     lib = "/tmp/libskei_stats.so"
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
                     "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
-                    "-DSKEI_FWD_STATS", "-I", os.path.join(ROOT, "include"), "-o", lib,
+                    "-DSKEI_FWD_STATS", *os.environ.get("STATS_FLAGS", "").split(), "-I", os.path.join(ROOT, "include"), "-o", lib,
                     *sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))], check=True)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
                           "--warmup", "3", "--no-cpu-baseline", "--no-e2e"],
@@ -39,7 +39,8 @@ def main():
         r = seen[w]
         print(f"cta {r[0]} warp {w:2d} units {r[2]} blocks {r[3]} wait {r[4]:7d} pro {r[5]:6d} "
               f"epi {r[6]:6d} compute {r[7] - r[4] - r[5] - r[6]:7d} total {r[7]} "
-              f"active tasks {r[8]} lanes/task {r[9] / max(1, r[8]):.1f}")
+              f"active tasks {r[8]} lanes/task {r[9] / max(1, r[8]):.1f}"
+              + (f" esync {r[10]} fin {r[11]}" if len(r) > 11 else ""))
 
 
 if __name__ == "__main__":
