@@ -23,6 +23,14 @@ def _need_cuda():
     torch.cuda.set_device(0)
 
 
+def _oracle_images(cfg, x1n, yn):
+    """The oracle's pass (fp64) for the images it checks: the first and last of the batch
+    (cfg2), the single image of cfg5 (same draw as the device's)."""
+    og, oidx = oracle.draw(0, 0, oracle.SHARED_IMAGE, cfg.n_full, cfg.m)
+    images = sorted({0, cfg.B - 1})
+    return {b: oracle.sketched_pass(x1n[b], yn[b], og, oidx, cfg.n_full) for b in images}
+
+
 def _close(got, ref, name):
     got = got.double().cpu().numpy() if torch.is_tensor(got) else np.asarray(got, np.float64)
     ref = ref.double().cpu().numpy() if torch.is_tensor(ref) else np.asarray(ref, np.float64)
@@ -58,11 +66,13 @@ def test_angle_shard_partials_sum_to_full_pass(name, world):
     _close(mc, full["mc"], "mc")
     ei = ops.ei(x2, xfbp, idx)
     _close(ei, full["ei"], "ei")
-    # and against the oracle for the first image (sampled rows of x_fbp, all of mc)
-    og, oidx = oracle.draw(0, 0, oracle.SHARED_IMAGE, cfg.n_full, cfg.m)
-    ref = oracle.sketched_pass(x1n[0], yn[0], og, oidx, cfg.n_full)
-    _close(xfbp[0], ref["xfbp"], "xfbp vs oracle")
-    _close(mc[0:1], np.array([ref["mc"]]), "mc vs oracle")
+    # and against the oracle directly: the shard partials summed in rank order are the
+    # oracle's full-sketch x_fbp, MC gradient, mc and ei (the partition identity)
+    for b, ref in _oracle_images(cfg, x1n, yn).items():
+        _close(xfbp[b], ref["xfbp"], f"xfbp[{b}] vs oracle")
+        _close(grad[b], ref["grad"], f"grad[{b}] vs oracle")
+        _close(mc[b:b + 1], np.array([ref["mc"]]), f"mc[{b}] vs oracle")
+        _close(ei[b:b + 1], np.array([ref["ei"]]), f"ei[{b}] vs oracle")
 
 
 def test_angle_split_pass_single_rank_equals_pass():
@@ -103,6 +113,24 @@ def test_allgather_split_bands_tile_full_pass(name, world):
     _close(torch.cat([b["grad"] for b in bands], dim=1), full["grad"], "grad bands")
     _close(sum(s["mc"] for s in shards), full["mc"], "mc")
     _close(sum(b["ei"] for b in bands), full["ei"], "ei")
+    # the bands tile the oracle's x_fbp and grad, the shards' mc and the bands' ei partials
+    # sum to the oracle's (the partition identity)
+    _check_split_vs_oracle(cfg, x1n, yn, bands, sum(s["mc"] for s in shards),
+                           sum(b["ei"] for b in bands))
+
+
+def _check_split_vs_oracle(cfg, x1n, yn, bands, mc, ei):
+    xf = torch.cat([bd["xfbp"] for bd in bands], dim=1)
+    gr = torch.cat([bd["grad"] for bd in bands], dim=1)
+    for b, ref in _oracle_images(cfg, x1n, yn).items():
+        for bd in bands:
+            rows = bd["rows"]
+            _close(bd["xfbp"][b], ref["xfbp"][rows.start:rows.stop], f"xfbp band {rows}[{b}] vs oracle")
+            _close(bd["grad"][b], ref["grad"][rows.start:rows.stop], f"grad band {rows}[{b}] vs oracle")
+        _close(xf[b], ref["xfbp"], f"xfbp[{b}] vs oracle")
+        _close(gr[b], ref["grad"], f"grad[{b}] vs oracle")
+        _close(mc[b:b + 1], np.array([ref["mc"]]), f"mc[{b}] vs oracle")
+        _close(ei[b:b + 1], np.array([ref["ei"]]), f"ei[{b}] vs oracle")
 
 
 def test_allgather_split_single_rank_equals_pass():
@@ -141,6 +169,13 @@ def test_p2p_fused_allgather_split_tiles_full_pass(name, world):
     _close(torch.cat([bd["grad"] for bd in bands], dim=1), full["grad"], "grad bands")
     _close(out["mc"], full["mc"], "mc")
     _close(sum(bd["ei"] for bd in bands), full["ei"], "ei")
+    # every rank's gathered q and r against the oracle's ramp of the full sketch and its
+    # residual rows; the bands, mc and ei against the oracle's pass
+    for b, ref in _oracle_images(cfg, x1n, yn).items():
+        for bf in out["bufs"]:
+            _close(bf[0][b], ref["q"], f"q[{b}] in a rank's buffer vs oracle")
+            _close(bf[1][b], ref["r"], f"r[{b}] in a rank's buffer vs oracle")
+    _check_split_vs_oracle(cfg, x1n, yn, bands, out["mc"], sum(bd["ei"] for bd in bands))
 
 
 def test_p2p_split_single_rank_equals_pass():

@@ -208,11 +208,44 @@ def test_pass_parity_small_configs(name, mode):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
-def test_pass_parity_full_size(name):
+@pytest.mark.parametrize("mode", [sk.MODE_UNIFORM, sk.MODE_INTERLEAVED])
+def test_pass_parity_full_size(name, mode):
     """BASELINE.json's full sizes in the bench's launch configuration (whole batch on the
-    GPU); the oracle recomputes the first and last image of the batch in full."""
+    GPU), in both sketch modes (north_star's uniform subset and the paper's interleaved
+    minibatches); the oracle recomputes, in full, the first, second, a middle and the
+    last image of the batch (each of its own image group of the projector)."""
     cfg = synth.CONFIGS[name]
-    _check_pass(cfg, sorted({0, cfg.B - 1}))
+    _check_pass(cfg, sorted({0, 1, cfg.B // 2, cfg.B - 1} & set(range(cfg.B))), mode)
+
+
+def _boundary_sketch(n_full, m, seed=0):
+    """A uniform draw of m angles forced to contain the class-boundary angles 0, 45, 90 and
+    135 degrees (indices 0, n_full/4, n_full/2, 3 n_full/4): the projector's row / column
+    class test is exact there (|cos| = |sin| at 45 and 135 degrees, zero sin / cos at 0 and
+    90), and the bin-pair windows reach their widest (|beta| = 1/sqrt 2)."""
+    _, idx = oracle.draw(seed, 5, SH, n_full, m)
+    must = [0, n_full // 4, n_full // 2, 3 * n_full // 4]
+    rest = [i for i in idx if i not in must][: m - len(must)]
+    return np.array(sorted(must + rest), np.int32)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("g", [45, 90, 137])
+def test_pass_parity_full_size_class_boundary_angles(g):
+    """cfg3 (N = 512) with a sketch holding 0/45/90/135 degrees; images 0, 5, 10 and 15
+    (one of each image group of the projector) against the oracle."""
+    cfg = synth.CONFIGS["cfg3"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1, y = synth.make_workload(cfg, 0)
+    idx = _boundary_sketch(cfg.n_full, cfg.m)
+    out = sk.sketched_pass(plan, dev(x1), dev(y), idx_t([g]), idx_t(idx[None]))
+    torch.cuda.synchronize()
+    for b in (0, 5, 10, 15):
+        ref = oracle.sketched_pass(x1[b], y[b], g, idx, cfg.n_full)
+        for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad"):
+            close(out[k][b], ref[k], f"boundary g={g} {k} b={b}")
+        for k in ("mc", "ei"):
+            assert abs(float(out[k][b]) - ref[k]) <= TOL * abs(ref[k]), (k, b)
 
 
 @pytest.mark.parametrize("N,n_det,n_full,P,B,m", [

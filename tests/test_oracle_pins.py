@@ -27,6 +27,76 @@ def test_splitmix64_reference_vector(golden_dir):
     assert [oracle.word(1234567, i) for i in range(5)] == vals
 
 
+# SURVEY §8(c) O-1 written out in plain Python integers (mod 2^64), independently of both C
+# implementations (oracle/oracle.c and the library's csrc/sm64.h): the key chain, the
+# multiply-high range reduction U(n) and the partial Fisher-Yates word order.
+_M64 = (1 << 64) - 1
+_GAMMA = 0x9E3779B97F4A7C15
+_STREAM_ROT, _STREAM_SKETCH = 1, 2
+
+
+def _o1_mix(z):
+    z = (z + _GAMMA) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _o1_key(seed, stream, it, image):
+    return _o1_mix(_o1_mix(_o1_mix(_o1_mix(seed) ^ stream) ^ it) ^ image)
+
+
+def _o1_word(key, i):
+    return _o1_mix((key + i * _GAMMA) & _M64)
+
+
+def _o1_u(w, n):
+    return (w * n) >> 64  # floor(w n / 2^64)
+
+
+def _o1_draw(seed, it, image, n_full, m, mode):
+    kr = _o1_key(seed, _STREAM_ROT, it, image)
+    g = 1 + _o1_u(_o1_word(kr, 0), 360)
+    ks = _o1_key(seed, _STREAM_SKETCH, it, image)
+    if mode == oracle.MODE_INTERLEAVED:
+        step = n_full // m
+        b = _o1_u(_o1_word(ks, 0), step)
+        return g, [b + k * step for k in range(m)]
+    perm = list(range(n_full))
+    for i in range(m):
+        j = i + _o1_u(_o1_word(ks, i), n_full - i)
+        perm[i], perm[j] = perm[j], perm[i]
+    return g, sorted(perm[:m])
+
+
+def test_o1_mix_is_splitmix64_stream():
+    """The i-th word of key k is the i-th output of a standard SplitMix64 generator seeded with
+    k; the published vector (seed 1234567) pins the finaliser and the increment order."""
+    vals = [int(l) for l in open(os.path.join(os.path.dirname(__file__), "golden",
+                                              "splitmix64_seed1234567.txt"))
+            if l.strip() and not l.startswith("#")]
+    assert [_o1_word(1234567, i) for i in range(5)] == vals
+
+
+@pytest.mark.parametrize("seed,it,image", [(0, 0, SH), (0, 1, SH), (0, 17, SH), (1, 0, 0),
+                                           (7, 11, 3), (12345, 999, SH), (2**63 + 5, 2, 63),
+                                           (0, 0, 0), (0, 0, 1), (3, 4, 2**32 + 1)])
+@pytest.mark.parametrize("n_full,m", [(32, 8), (128, 32), (360, 90), (720, 180), (1024, 256),
+                                      (12, 12), (5, 1)])
+def test_o1_draw_rederived_in_python_integers(seed, it, image, n_full, m):
+    """oracle.draw equals O-1 re-derived here in Python integers: the key chain
+    mix(mix(mix(mix(seed) ^ stream) ^ iter) ^ image), U(n) = floor(w n / 2^64), g from word 0
+    of ROT, the interleaved offset from word 0 of SKETCH and the Fisher-Yates target of step i
+    from word i."""
+    for mode in (oracle.MODE_UNIFORM, oracle.MODE_INTERLEAVED):
+        if mode == oracle.MODE_INTERLEAVED and n_full % m:
+            continue
+        g, idx = oracle.draw(seed, it, image, n_full, m, mode)
+        rg, ridx = _o1_draw(seed, it, image, n_full, m, mode)
+        assert g == rg and list(idx) == ridx, (mode, g, rg)
+    assert oracle.key(seed, _STREAM_SKETCH, it, image) == _o1_key(seed, _STREAM_SKETCH, it, image)
+
+
 def test_interleave_rule_examples():
     """SPEC S:164 example (4 angles, 2 minibatches) -> [[0,2],[1,3]]
     'interleaved angles'; and the (100, 10) example S:165: batch i = {i, i+10, ..., i+90}."""
