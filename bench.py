@@ -8,21 +8,30 @@ one batch of config 3 (512x512 fp32, B = 16, 360 angles, 725 bins, m = 90 unifor
 P = 2048), inputs resident in HBM, L2 flushed (256 MB write) before every timed step, each
 step timed with CUDA events on the launching stream.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl skei|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl skei|reference] [--config cfgN]
 
-Multi-GPU (torchrun, one rank per GPU): the path partitions by image batch, so every rank
-runs its own config-3 batch (weak scaling, no data-path collective); value = N*K passes /
-max-over-ranks device time.  `--impl reference` times the fp64 oracle (the only reference
-this paper-only tier has) on the host cores on a bounded sample of the same workload.
+Multi-GPU: one rank per GPU.  Launched by torchrun (RANK / LOCAL_RANK / WORLD_SIZE in the
+environment) or, when `--gpus N > 1` is given without them, bench.py re-launches itself
+under `torch.distributed.run` with N ranks on this node (127.0.0.1).  The path partitions
+by image batch with no data-path collective: for config 3 (the headline) every rank runs
+its own 16-image batch (weak scaling, value = N*K passes / max-over-ranks device time);
+for config 4 ("batch 64 split by batch across 1/2/4/8 GPUs") the 64 images are split
+64/N per rank, draws keyed by the global image index (strong scaling, value = K whole
+64-image passes / max-over-ranks device time).  `--impl reference` times the fp64 oracle
+(the only reference this paper-only tier has) on the host cores, whole passes.
 """
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -31,8 +40,74 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-METRIC = "sketched EI operator passes/s at 512², 360→90 angles; % HBM/gather roofline"
 UNIT = "passes/s"
+# configs whose batch is split over the ranks (strong scaling; BASELINE.json cfg4 "batch 64
+# split by batch across 1/2/4/8 GPUs"); every other config runs one batch per rank (weak)
+STRONG_BATCH = {"cfg4"}
+HBM_FALLBACK_GBS = 6548.8  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def metric_of(cfg):
+    """BASELINE.json's metric, written for the config it is measured on."""
+    return (f"sketched EI operator passes/s at {cfg.N}², {cfg.n_full}→{cfg.m} angles; "
+            f"% HBM/gather roofline")
+
+
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's driver-measured copy bandwidth, else the guide's
+    fallback."""
+    try:
+        v = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+
+
+def host_cpu():
+    """(logical cores, model name) of this host (lscpu's 'Model name' = /proc/cpuinfo)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args):
+    """`--gpus N` with N > 1 outside torchrun: re-run this script under torch.distributed.run
+    with N ranks (one per GPU), rendezvous on 127.0.0.1; rank 0 prints the JSON line.
+    Returns the launcher's exit code, or None when this process is already a rank."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if args.gpus is not None and int(world_env) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}\n")
+            return 2
+        return None
+    if (args.gpus or 1) <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def rank_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SKEI_BENCH_RANKINFO"):  # launcher test: every rank reports its env
+        sys.stderr.write(f"rankinfo rank={rank} local={local} world={world}\n")
+        sys.stderr.flush()
+    return world, rank, local
 # stage boundaries recorded by skei_pass_profiled: 0 start | rotate+pack | 1 | forward x2
 # (+ fused MC residual) | 2 | ramp | 3 | backprojection x2 (+ fused EI residual) | 4 | 5 end
 STAGES = ["rotate_pack", "radon_fwd_x2", "ramp", "radon_adj_x2"]
@@ -43,7 +118,8 @@ L2_FLUSH_BYTES = 256 << 20
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); default: WORLD_SIZE under torchrun, else 1")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
@@ -65,6 +141,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-grad", action="store_true",
+                    help="the e2e leg also reads the MC gradient back every step (D2H of B N^2 "
+                         "fp32, besides mc / ei)")
     return ap.parse_args()
 
 
@@ -142,48 +221,99 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_sample(cfg, seconds, mode, seed=0):
-    """Time the fp64 oracle (as it stands, single-threaded) on whole images of the workload
-    until ~`seconds` of CPU work; returns (passes/s, images, elapsed)."""
+def oracle_draws(cfg, mode, seed, it):
+    """The pass's draws as the oracle computes them: one shared (g, S), or one per image
+    (cfg4), keyed by the global image index."""
     import oracle
-    x1, y = synth.make_workload(cfg, seed, images=range(1))
     md = 1 if mode == "uniform" else 0
-    g, idx = oracle.draw(seed, 0, oracle.SHARED_IMAGE, cfg.n_full, cfg.m, md)
-    t0 = time.perf_counter()
-    n = 0
-    while True:
-        oracle.sketched_pass(x1[0], y[0], g, idx, cfg.n_full)
+    if cfg.per_image_draws:
+        return [oracle.draw(seed, it, b, cfg.n_full, cfg.m, md) for b in range(cfg.B)]
+    return [oracle.draw(seed, it, oracle.SHARED_IMAGE, cfg.n_full, cfg.m, md)] * cfg.B
+
+
+def oracle_pass_batch(cfg, x1, y, draws, threads):
+    """One whole pass of the batch through the fp64 oracle as it stands (oracle.c via
+    ctypes, which releases the GIL): images in turn (threads = 1) or spread over `threads`
+    host threads."""
+    import oracle
+
+    def one(b):
+        g, idx = draws[b]
+        oracle.sketched_pass(x1[b], y[b], g, idx, cfg.n_full)
+
+    if threads <= 1:
+        for b in range(cfg.B):
+            one(b)
+    else:
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(cfg.B)))
+
+
+def cpu_baseline_legs(cfg, mode, seed, seconds):
+    """SURVEY §8(d)'s CPU baseline: the oracle timed on this host's cores on whole passes of
+    the workload's batch, (i) single-threaded (a bounded sample of images if one pass would
+    exceed `seconds`) and (ii) one thread per logical core over the images.  Returns the
+    cpu_baseline object (value = the all-cores leg)."""
+    cores, model = host_cpu()
+    x1, y = synth.make_workload(cfg, seed)
+    draws = oracle_draws(cfg, mode, seed, 0)
+    import oracle
+    t0, n = time.perf_counter(), 0
+    while True:  # (i) single thread, image by image
+        g, idx = draws[n % cfg.B]
+        oracle.sketched_pass(x1[n % cfg.B], y[n % cfg.B], g, idx, cfg.n_full)
         n += 1
         el = time.perf_counter() - t0
-        if el >= seconds or el / n * (n + 1) > 1.5 * seconds:
+        if n >= cfg.B or el >= seconds or el / n * (n + 1) > 1.5 * seconds:
             break
-    return (n / cfg.B) / el, n, el
+    single = (n / cfg.B) / el
+    threads = min(cores, cfg.B)
+    t0, npass = time.perf_counter(), 0
+    while True:  # (ii) whole passes, images spread over the host's cores
+        oracle_pass_batch(cfg, x1, y, draws, threads)
+        npass += 1
+        el2 = time.perf_counter() - t0
+        if el2 >= 0.5 * seconds or npass >= 3:
+            break
+    return {"value": npass / el2, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "host_cores": cores, "cpu_model": model,
+            "single_core": {"value": single, "unit": UNIT, "cores": 1,
+                            "sample": f"{n} image(s) of the batch, one at a time ({el:.1f} s)"},
+            "sample": f"{npass} whole {cfg.name} pass(es) ({cfg.B} images each) through the fp64 "
+                      f"oracle, one host thread per image up to {threads} threads ({el2:.1f} s); "
+                      f"the oracle's ramp is its direct O(n_det^2) convolution"}
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
+    """--impl reference: the fp64 oracle as it stands on this host's cores, every step one
+    whole pass of the config's batch (its images spread over one thread per core); rank 0
+    only under torchrun (the other ranks exit 0 without work)."""
+    world, rank, _ = rank_env()
     if rank != 0:
         return 0
-    import oracle
     cfg = synth.CONFIGS[args.config]
-    x1, y = synth.make_workload(cfg, args.seed, images=range(1))
-    md = 1 if args.mode == "uniform" else 0
+    cores, model = host_cpu()
+    threads = min(cores, cfg.B)
+    x1, y = synth.make_workload(cfg, args.seed)
     times = []
     for i in range(args.warmup + args.steps):
-        g, idx = oracle.draw(args.seed, i, oracle.SHARED_IMAGE, cfg.n_full, cfg.m, md)
+        draws = oracle_draws(cfg, args.mode, args.seed, i)
         t0 = time.perf_counter()
-        oracle.sketched_pass(x1[0], y[0], g, idx, cfg.n_full)
+        oracle_pass_batch(cfg, x1, y, draws, threads)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
-    per_image = float(np.mean(times))
-    value = 1.0 / (per_image * cfg.B)
-    sample = f"each step = the full pass on 1 of the {cfg.B} images of a {cfg.name} batch (1/{cfg.B} pass)"
+    ms = float(np.mean(times)) * 1e3
+    value = 1e3 / ms
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_image * cfg.B * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_desc(cfg, args.mode),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "impl": "reference", "metric": metric_of(cfg), "value": value, "unit": UNIT,
+        "n_gpus": args.gpus or world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if cfg.name in STRONG_BATCH else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg, args.mode),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "host_cores": cores, "cpu_model": model,
+                         "sample": f"every step = one whole {cfg.name} pass ({cfg.B} images, fresh "
+                                   f"draw per step) through the fp64 oracle, {threads} host threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,9 +331,7 @@ def run_angle(args):
     import paper_2411_05771_b200 as sk
     from paper_2411_05771_b200 import dist as skdist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = rank_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -221,8 +349,14 @@ def run_angle(args):
     split_fn = {"angle-ag": skdist.angle_split_pass_allgather,
                 "angle-p2p": skdist.angle_split_pass_p2p}.get(args.split, skdist.angle_split_pass)
 
+    # the P2P split's symmetric-memory buffers are allocated (and rendezvoused) once, outside
+    # the timed loop
+    p2p = skdist.P2PBuffers(cfg.B, cfg.m, cfg.n_det, dev) if args.split == "angle-p2p" else None
+
     def step(it):
         g, idx = sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, cfg.m, mode)
+        if p2p is not None:
+            return split_fn(ops, x1, y, g, idx[0], bufs=p2p)
         return split_fn(ops, x1, y, g, idx[0])
 
     for i in range(args.warmup):
@@ -275,6 +409,8 @@ def run_ei_grad(args):
     x_fbp come from one pass; one CUDA graph per step (5 launches), L2 flushed before every
     timed step, CUDA events.  The oracle (oracle.ei_grad, fp64, 1 core) is timed on a
     bounded sample of images."""
+    if rank_env()[1] != 0:  # a one-GPU diagnostic: only rank 0 runs it
+        return 0
     import torch
 
     import paper_2411_05771_b200 as sk
@@ -351,6 +487,8 @@ def run_rei(args):
     max|y| (the config's noise level), fresh draw and noise stream every step (graphed per
     step: draw + 6 launches), L2 flushed before every timed step, CUDA events; oracle REI
     pass timed beside it on a bounded sample."""
+    if rank_env()[1] != 0:  # a one-GPU diagnostic: only rank 0 runs it
+        return 0
     import torch
 
     import paper_2411_05771_b200 as sk
@@ -424,6 +562,8 @@ def run_deviation(args):
     (interleaved sketches), `--steps` power iterations each from a random start image; the
     timed unit is one power iteration (2 forward projections: all n_full angles and the
     sketch, 2 backprojections, 1 norm), CUDA events, one stream."""
+    if rank_env()[1] != 0:  # a one-GPU diagnostic: only rank 0 runs it
+        return 0
     import torch
 
     import paper_2411_05771_b200 as sk
@@ -472,6 +612,9 @@ def run_deviation(args):
 
 def main():
     args = parse()
+    rc = launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.path == "deviation":
         return run_deviation(args)
     if args.impl == "reference":
@@ -490,9 +633,7 @@ def main():
 
     import paper_2411_05771_b200 as sk
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = rank_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -501,11 +642,18 @@ def main():
     cfg = synth.CONFIGS[args.config]
     mode = sk.MODE_UNIFORM if args.mode == "uniform" else sk.MODE_INTERLEAVED
     shared = not cfg.per_image_draws
-    B, m, N = cfg.B, cfg.m, cfg.N
+    m, N = cfg.m, cfg.N
+    # this rank's images (global indices): a share of the config's batch (strong scaling,
+    # cfg4) or a whole batch of its own (weak scaling, rank r: images r B ... r B + B - 1)
+    strong = cfg.name in STRONG_BATCH
+    from paper_2411_05771_b200.dist import batch_range
+    images = batch_range(cfg.B, rank, world) if strong else range(rank * cfg.B, (rank + 1) * cfg.B)
+    B, img0 = len(images), images.start
+    lcfg = dataclasses.replace(cfg, B=B)  # the work one rank does per step
     plan = sk.Plan.get(N, cfg.n_det, cfg.n_full, cfg.fft_len, device=local)
 
-    # inputs: this rank's images (global indices rank*B ...), resident in HBM
-    x1_np, y_np = synth.make_workload(cfg, args.seed, images=range(rank * B, (rank + 1) * B))
+    # inputs: this rank's images, resident in HBM
+    x1_np, y_np = synth.make_workload(cfg, args.seed, images=images)
     x1 = torch.from_numpy(x1_np).to(dev)
     y = torch.from_numpy(y_np).to(dev)
     out = sk.alloc_pass_outputs(plan, B, m, dev)
@@ -517,10 +665,10 @@ def main():
 
     def step(it, events, fused=True):
         if fused:  # the timed form: one call, the draw overlapped with packing x1
-            sk.sketched_pass_draw(plan, x1, y, args.seed, it, m, mode, shared, rank * B, g=gbuf,
+            sk.sketched_pass_draw(plan, x1, y, args.seed, it, m, mode, shared, img0, g=gbuf,
                                   idx=ibuf, out=out, ws=ws, events=events)
             return
-        sk.draw_device(args.seed, it, rank * B, 1 if shared else B, shared, cfg.n_full, m, mode,
+        sk.draw_device(args.seed, it, img0, 1 if shared else B, shared, cfg.n_full, m, mode,
                        g=gbuf, idx=ibuf)
         sk.sketched_pass_profiled(plan, x1, y, gbuf, ibuf, events, out, ws)
 
@@ -549,9 +697,14 @@ def main():
             step(it, events, fused)
         return gr
 
-    graphs = [capture(i * world + rank, fwd_events[i]) for i in range(n_iter)]
+    # pass index of step i: the same on every rank for a split batch (one pass of the whole
+    # batch), distinct per rank for independent batches
+    def pass_it(i):
+        return i if strong else i * world + rank
+
+    graphs = [capture(pass_it(i), fwd_events[i]) for i in range(n_iter)]
     # the breakdown graphs launch the draw and the pass separately (each stage alone)
-    brk_graphs = [capture((n_iter + i) * world + rank, brk_events[i], False) for i in range(n_brk)]
+    brk_graphs = [capture(pass_it(n_iter + i), brk_events[i], False) for i in range(n_brk)]
     torch.cuda.synchronize()
     for i in range(args.warmup):
         graphs[i].replay()
@@ -602,7 +755,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * args.steps / (total_ms * 1e-3)
+    passes_per_step = 1 if strong else world  # whole passes the job completes per step
+    value = passes_per_step * args.steps / (total_ms * 1e-3)
+    # up to 10 windows of consecutive timed steps (this rank's times)
+    wins = [w for w in np.array_split(step_ms, min(10, args.steps)) if len(w)]
+    win_vals = [passes_per_step * len(w) / (w.sum() * 1e-3) for w in wins]
 
     # ---- end to end through the public host-buffer call (skei_pass_host).  E2E_SLOTS slots
     # (device inputs/outputs, workspace, pinned draw/staging/result buffers, stream) rotate, so
@@ -626,6 +783,7 @@ def main():
                               hidx=torch.empty(ng, m, dtype=torch.int32).pin_memory(),
                               hmc=torch.empty(B).pin_memory(), hei=torch.empty(B).pin_memory(),
                               ys=torch.empty(B, m, cfg.n_det).pin_memory() if shared else None,
+                              hgrad=torch.empty(B, N, N).pin_memory() if args.e2e_grad else None,
                               done=None, fl=torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)))
         results = []
 
@@ -635,13 +793,15 @@ def main():
                 sl["done"].synchronize()
                 results.append(float(sl["hmc"][0]))
             for b in range(ng):  # host draw (skei_draw)
-                gi, ii = sk.draw(args.seed, it, sk.SHARED_IMAGE if shared else rank * B + b,
+                gi, ii = sk.draw(args.seed, it, sk.SHARED_IMAGE if shared else img0 + b,
                                  cfg.n_full, m, mode)
                 sl["hg"][b] = gi
                 sl["hidx"][b] = torch.tensor(ii, dtype=torch.int32)
             with torch.cuda.stream(sl["st"]):
                 sk.sketched_pass_host(plan, hx1, hy, sl["hg"], sl["hidx"], sl["d"], sl["hmc"],
                                       sl["hei"], sl["ws"], sl["fl"], h_ystage=sl["ys"])
+                if sl["hgrad"] is not None:  # the MC gradient back to the host as well
+                    sl["hgrad"].copy_(sl["d"]["grad"], non_blocking=True)
                 # L2 flush behind the pass in the same stream (so it never holds up the next
                 # step's H2D on the other stream): this slot's next pass starts cold
                 sl["fl"].zero_()
@@ -666,14 +826,18 @@ def main():
         # a shared sketch copies only y's m sketched rows (skei_pass_host), else all of y
         y_h2d = B * m * cfg.n_det * 4 if shared else hy.numel() * 4
         h2d = hx1.numel() * 4 + y_h2d + ng * 4 + ng * m * 4
-        e2e = {"value": world * args.steps / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(2 * B * 4),
+        d2h = 2 * B * 4 + (B * N * N * 4 if args.e2e_grad else 0)
+        e2e = {"value": passes_per_step * args.steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "returns": "mc, ei and the MC gradient" if args.e2e_grad else
+                          "mc, ei (the gradient and x_fbp stay on the device; --e2e-grad reads "
+                          "the gradient back too)",
                "timing": "host wall clock over all steps; per step: host draw, H2D of x1, y_S "
                          "(the sketched rows of y gathered into a pinned staging buffer by the "
                          "library; all of y for per-image sketches), g, idx "
-                         "from pinned memory, the pass, D2H of mc/ei, in-stream L2 flush (256 MB "
-                         "write) behind it; slots with their own streams rotate, so one step's H2D overlaps "
-                         "the previous steps' passes (3 slots)"}
+                         "from pinned memory, the pass, D2H of its results, in-stream L2 flush "
+                         "(256 MB write) behind it; slots with their own streams rotate, so one "
+                         "step's H2D overlaps the previous steps' passes (3 slots)"}
 
     if rank != 0:
         if world > 1:
@@ -697,8 +861,9 @@ def main():
             traffic = json.load(open(tf)).get(dname)
         except Exception:
             traffic = None
-    t_gather = 4.0 * taps_per_pass(cfg) / (peak * 1e9)
-    t_hbm = hbm_bytes_per_pass(cfg) / (6548.8e9)
+    hbm_gbs, hbm_src = hbm_peak()
+    t_gather = 4.0 * taps_per_pass(lcfg) / (peak * 1e9)
+    t_hbm = hbm_bytes_per_pass(lcfg) / (hbm_gbs * 1e9)
     pass_frac = max(t_gather, t_hbm) / (ms_per_step * 1e-3)
     roofline = {
         "bound": "smem", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -709,28 +874,36 @@ def main():
                        f"(2 jobs x {B} images x {m} angles x {N}^2 px x 2 taps)",
         "kernel_ms": float(fwd_ms.mean()),
         "pass_frac": pass_frac,
-        "pass_roofline": f"max(T_gather = 4 B x {taps_per_pass(cfg):.4g} taps / peak, T_hbm = "
-                         f"{hbm_bytes_per_pass(cfg):.4g} B / 6548.8 GB/s) / measured step time",
+        "pass_roofline": f"max(T_gather = 4 B x {taps_per_pass(lcfg):.4g} taps / peak, T_hbm = "
+                         f"{hbm_bytes_per_pass(lcfg):.4g} B / {hbm_gbs:g} GB/s ({hbm_src})) / "
+                         f"measured step time (one rank's {B} images)",
     }
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v, nimg, el = oracle_sample(cfg, args.cpu_seconds, args.mode, args.seed)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{nimg} image(s) of a {cfg.name} batch through the fp64 oracle pass "
-                         f"({el:.1f} s; {cfg.B} images = 1 pass)"}
+        cpu = cpu_baseline_legs(cfg, args.mode, args.seed, args.cpu_seconds)
 
+    desc = workload_desc(cfg, args.mode)
+    desc["images_per_gpu"] = B
+    if world > 1 or strong:
+        desc["parallelism"] = (f"batch split x{world}: {cfg.B} images, {B} per rank, draws keyed "
+                               f"by the global image index, no data-path collective" if strong else
+                               f"batch x{world}: every rank its own {cfg.B}-image batch, no "
+                               f"data-path collective")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_desc(cfg, args.mode),
+        "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": desc,
+        "windows": {"n": len(win_vals), "median": float(np.median(win_vals)),
+                    "min": float(np.min(win_vals)), "max": float(np.max(win_vals)),
+                    "unit": UNIT, "rank": "rank 0's step times"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk.summary(),
         "stages_ms": {**{"draw": float(draw_ms.mean())},
                       **{s: float(v) for s, v in zip(STAGES, stage_mean)}},
-        "images_per_s": value * B,
+        "images_per_s": value * (cfg.B if strong else B),
         "taps_per_s": taps_per_pass(cfg) * value,
     }
     print(json.dumps(line), flush=True)

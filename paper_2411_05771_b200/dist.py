@@ -245,10 +245,11 @@ class P2PBuffers:
             self.peer_r = [self.buf[1].data_ptr()]
         self.q, self.r = self.buf[0], self.buf[1]
 
-    def barrier(self):
-        """Every rank's stores have landed in every buffer (stream-ordered device barrier)."""
+    def barrier(self, channel: int = 0):
+        """Stream-ordered device barrier over the group: every rank's stream has reached
+        this point (e.g. its stores have landed in every buffer)."""
         if self.handle is not None:
-            self.handle.barrier(channel=0)
+            self.handle.barrier(channel=channel)
 
 
 def angle_split_pass_p2p(ops, x1, y, g, idx, group=None, bufs: P2PBuffers | None = None):
@@ -267,6 +268,10 @@ def angle_split_pass_p2p(ops, x1, y, g, idx, group=None, bufs: P2PBuffers | None
     B, n_det = p2.shape[0], p2.shape[-1]
     if bufs is None:
         bufs = P2PBuffers(B, m, n_det, p2.device, group)
+    else:
+        # reused buffers: no rank may overwrite a peer's q / r while that peer still
+        # backprojects the previous pass from them (write-after-read across ranks)
+        bufs.barrier(channel=1)
     ops.ramp_allgather(p2, r, row0, m, bufs.peer_q, bufs.peer_r)
     bufs.barrier()
     bd = band_phase(ops, bufs.q, bufs.r, idx, x2, rank, world)

@@ -38,3 +38,44 @@ def test_reference_arm_other_ranks_exit_quietly():
     out = _run({"RANK": "1", "WORLD_SIZE": "2"})
     assert out.returncode == 0, out.stderr[-2000:]
     assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def _clean_env(extra=None):
+    e = {k: v for k, v in os.environ.items()
+         if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    e.update(extra or {})
+    return e
+
+
+def test_gpus_flag_launches_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run:
+    two processes with RANK / LOCAL_RANK 0 and 1 and WORLD_SIZE 2; only rank 0 prints the
+    JSON line, which reports n_gpus = 2."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                          "reference", "--config", "cfg1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=_clean_env({"SKEI_BENCH_RANKINFO": "1"}))
+    assert out.returncode == 0, out.stderr[-2000:]
+    info = sorted(l.split()[1:] for l in out.stderr.splitlines() if l.startswith("rankinfo"))
+    assert info == [["rank=0", "local=0", "world=2"], ["rank=1", "local=1", "world=2"]], out.stderr
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpus_flag_must_match_world_size():
+    out = _run({"RANK": "0", "WORLD_SIZE": "2"}, "--gpus", "4")
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
+
+
+def test_reference_arm_steps_fit_its_run_time():
+    """Every reference step is one whole pass of the batch: steps x ms_per_step is time the
+    process really spent (the driver's fits_in_driver_run check)."""
+    import time
+    t0 = time.perf_counter()
+    out = _run(_clean_env())
+    wall = time.perf_counter() - t0
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    assert d["steps"] * d["ms_per_step"] * 1e-3 <= wall
+    assert "whole" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["host_cores"] >= 1

@@ -48,3 +48,14 @@ def test_bench_json_line_contract():
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 5 * d["steps"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+def test_bench_cfg4_batch_split_line():
+    """BASELINE.json cfg4 ("batch 64 split by batch across 1/2/4/8 GPUs"): strong scaling,
+    per-image draws; at one GPU the rank holds all 64 images."""
+    d = _run("--config", "cfg4", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+             "--no-e2e", "--gpus", "1")
+    assert d["scaling"] == "strong" and d["n_gpus"] == 1
+    assert d["config"]["images_per_gpu"] == 64 and "720→180" in d["metric"]
+    assert abs(d["value"] * d["ms_per_step"] * 1e-3 - 1.0) < 1e-6
+    assert d["windows"]["n"] == 3 and d["windows"]["min"] <= d["windows"]["median"] <= d["windows"]["max"]
