@@ -68,6 +68,9 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
         const size_t f = pack_floats(plan, B, bb);
         if (f > pk) pk = f;
     }
+    // the job-fused copies (blocks of 16 lines x 2 jobs, one class) span two consecutive slots
+    const size_t fused = (size_t)B * ((plan->n + 15) / 16) * plan->n * 32;
+    if ((fused + 1) / 2 > pk) pk = (fused + 1) / 2;
     for (int i = 0; i < 4; ++i) {
         w.pack[i] = off;
         off += align256(sizeof(float) * pk);
@@ -563,10 +566,16 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
     // a2: x2 = T_g x1, fused with packing x1 and x2 for the forward projector (and zeroing
     // the completion counters of the fused reductions below)
+    // Images that cannot be grouped (per-image sketches, odd B) are projected job-fused: an
+    // image's x1 and x2 share its sketch, so they are the two slots of one group of the
+    // forward (one set of per-(bin, line) geometry for both), packed together: the fused
+    // row-packed copy spans pack[0..1], the column-packed one pack[2..3]
+    const bool fuse = fwd_bb(B, idx_stride) == 1;
     RotPackJob rj[2] = {
-        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), ctr},
-        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), nullptr}};
-    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s, draw != nullptr));
+        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[fuse ? 2 : 1]), ctr},
+        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[fuse ? 0 : 2]), ws_f(ws, wl.pack[fuse ? 2 : 3]),
+         nullptr}};
+    SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s, draw != nullptr, fuse));
     SKEI_CUDA(mark(1));
     // a3 + a7 (MC part): p1 = A_S x1 with r = p1 - y_S and mc = ||r||^2 fused into its
     // epilogue, and p2 = A_S x2, in one launch
@@ -574,11 +583,11 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     // padded layout (its windows are then one bulk copy per angle)
     const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
     float *qi = il ? ws_f(ws, wl.qi) : nullptr, *ri = il ? ws_f(ws, wl.ri) : nullptr;
-    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), o->p1, y, o->r, y_sketched},
+    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[fuse ? 2 : 1]), o->p1, y, o->r, y_sketched},
                     {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
     FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
-    SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr));
+    SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr, fuse));
     SKEI_CUDA(mark(2));
     // a4: q = ramp(p2); the same launch also copies r into the interleaved layout.  REI:
     // q = ramp(p2 + sigma eps), the noisy copy in the workspace (p2 stays noise-free)

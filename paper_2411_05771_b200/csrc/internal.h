@@ -65,9 +65,12 @@ struct RotPackArgs {
     const double2 *rot;  // plan->d_rot
     int n, B, nblk, tiles_c;
     int pdl;             // launched programmatically behind k_draw: the rotation job waits
+    int fuse;            // job-fused layout (bb = 1, 2 jobs): image b's x1 and x2 are the two
+                         // slots of group b, blocks of 16 lines: [b][blk][pixel][line][job]
 };
+// fuse: the job-fused packed layout (see RotPackArgs), for a forward launch with fused jobs
 cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
-                               int bb, cudaStream_t s, bool pdl = false);
+                               int bb, cudaStream_t s, bool pdl = false, bool fuse = false);
 cudaError_t launch_rotate(const skei_plan *plan, const float *x, float *out, int B,
                           const int32_t *g, int g_stride, cudaStream_t s);
 // out = T_g^T y (gather form of the rotation's transpose)
@@ -75,6 +78,8 @@ cudaError_t launch_rotate_adj(const skei_plan *plan, const float *y, float *out,
                               const int32_t *g, int g_stride, cudaStream_t s);
 
 // Forward projector on packed input; up to two jobs (e.g. A_S x1 and A_S x2) per launch.
+// fused: the two jobs of each image share its sketch and are processed as the two slots of
+// one group (the job-fused packed layout of launch_rotate_pack; jobs[0].xr / xc point to it).
 // Job 0 may fuse the MC residual: y != NULL -> r = p - y_S (if r != NULL) and mc = sum r^2.
 struct FwdJob {
     const float *xr, *xc;
@@ -97,7 +102,7 @@ size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride);
 size_t fwd_scratch_floats(const skei_plan *plan);
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, const FwdScratch &scr,
-                             cudaStream_t s, const FwdMc *mc = nullptr);
+                             cudaStream_t s, const FwdMc *mc = nullptr, bool fused = false);
 
 // Backprojection; up to two jobs sharing one angle list (FBP of q and gradient of r).
 // Job 0 may fuse ei = sum (x2 - x_job0)^2 (identity network): partial sums per tile.

@@ -88,7 +88,11 @@ struct FwdArgs {
     FwdJob job[2];
     int njobs;
     const int32_t *idx;
-    int m, idx_stride, B, nq;  // nq = image groups = B / BB
+    int m, idx_stride, B, nq;  // nq = image groups = B / BB (fused: B)
+    // job-fused groups (BB = 2): group q is image q, its slots 0 / 1 are job 0 / job 1 (x1 and
+    // x2 of one image share its sketch, so they share the projector's geometry); job[0].xr /
+    // xc hold the fused packed layout, slot b's projections go to job[b].p, MC on slot 0
+    int fused;
     int K;       // angles per unit: K * chunks <= kWarps * kMaxT tasks
     int chunks;  // ceil(n_det / 32)
     int nblk;    // packed blocks per image group (ceil(n / R))
@@ -204,7 +208,7 @@ __device__ __forceinline__ UnitId decode_unit(const Units &U, int nq, int K, int
     return d;
 }
 
-template <int BB>
+template <int BB, bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     constexpr int R = kColF / BB;
     constexpr int kMaxT = max_tasks<BB>();
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 
     // ---- 1. class sizes per image group -> unit table (identical in every CTA)
     for (int q = warp; q < nq; q += kWarps) {
-        const int32_t *iq = a.idx + (a.idx_stride ? (long)q * BB * a.idx_stride : 0);
+        const int32_t *iq = a.idx + (a.idx_stride ? (long)q * (FUSED ? 1 : BB) * a.idx_stride : 0);
         int cnt = 0;
         for (int base = 0; base < a.m; base += 32) {
             const int k = base + lane;
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #endif
         const UnitId d = decode_unit(U, nq, K, u);
         const FwdJob job = d.job ? a.job[1] : a.job[0];
-        const int b0 = d.q * BB;
+        const int b0 = FUSED ? d.q : d.q * BB;  // the group's first image (fused: its image)
         const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
 
         // ---- 2. the unit's K angles (grp-th group of class cls, sketch-slot order) + geometry
@@ -660,15 +664,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         float racc[BB];
 #pragma unroll
         for (int b = 0; b < BB; ++b) racc[b] = 0.f;
+        // slot b's projection image (fused: job b's output for image b0)
+        auto slot_p = [&](int b) -> float * {
+            return FUSED ? a.job[b].p + (long)b0 * img_stride : job.p + (long)(b0 + b) * img_stride;
+        };
         auto finish_bin = [&](int slot, int j, const float (&sv)[BB]) {
             const long pj = (long)slot * n_det + j;
 #pragma unroll
-            for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[b];
+            for (int b = 0; b < BB; ++b) slot_p(b)[pj] = sv[b];
             if (mc) {
                 const long yj = (long)(job.y_sketched ? slot : idx[slot]) * n_det + j;
                 const long ys = (long)(job.y_sketched ? a.m : n_full) * n_det;
 #pragma unroll
-                for (int b = 0; b < BB; ++b) {
+                for (int b = 0; b < (FUSED ? 1 : BB); ++b) {
                     const float dr = sv[b] - __ldg(job.y + (long)(b0 + b) * ys + yj);
                     if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
                     racc[b] = fmaf(dr, dr, racc[b]);
@@ -757,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             }
         }
         __syncthreads();  // s_red complete; s_task / sSlot free for the next unit
-        if (mc && finish && threadIdx.x < BB) {
+        if (mc && finish && threadIdx.x < (FUSED ? 1 : BB)) {
             float v = 0.f;
             for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
             a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
@@ -778,7 +786,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         if (u < 0) continue;
         const UnitId d = decode_unit(U, nq, K, u);
         const FwdJob job = d.job ? a.job[1] : a.job[0];
-        const int b0 = d.q * BB;
+        const int b0 = FUSED ? d.q : d.q * BB;
         const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
         __syncthreads();  // sSlot free
         if (warp == 0) {  // the unit's angle slots, as in step 2
@@ -842,10 +850,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const int k = o2 / n_det, j = o2 - k * n_det;
                 const long pj = (long)sSlot[k] * n_det + j;
 #pragma unroll
-                for (int b = 0; b < BB; ++b) job.p[(long)(b0 + b) * img_stride + pj] = sv[q][b];
+                for (int b = 0; b < BB; ++b)
+                    (FUSED ? a.job[b].p + (long)b0 * img_stride : job.p + (long)(b0 + b) * img_stride)[pj] = sv[q][b];
                 if (mc) {
 #pragma unroll
-                    for (int b = 0; b < BB; ++b) {
+                    for (int b = 0; b < (FUSED ? 1 : BB); ++b) {
                         const float dr = sv[q][b] - yv[q][b];
                         if (job.r) job.r[(long)(b0 + b) * img_stride + pj] = dr;
                         racc[b] = fmaf(dr, dr, racc[b]);
@@ -862,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 if (lane == 0) s_red[warp][b] = v;
             }
             __syncthreads();
-            if (threadIdx.x < BB) {
+            if (threadIdx.x < (FUSED ? 1 : BB)) {
                 float v = 0.f;
                 for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
                 a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
@@ -888,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     if (!s_last) return;
     __threadfence();
     for (int b = warp; b < a.B; b += kWarps) {
-        const int q = b / BB;
+        const int q = FUSED ? b : b / BB;
         const int ns = U.uoff[q + 1] - U.uoff[q];
         double sum = 0.0;
         for (int i = lane; i < ns; i += 32) sum += (double)__ldcg(a.mc_part + (long)b * a.mc_slots + i);
@@ -899,14 +908,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     if (threadIdx.x == 0) *a.mc_ctr = 0u;  // ready for the next launch
 }
 
-template <int BB>
+template <int BB, bool FUSED = false>
 cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     constexpr int R = kColF / BB;
     a.K = (kWarps * max_tasks<BB>()) / a.chunks;
     if (a.K > kKMax) a.K = kKMax;
     if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * kChunk
     a.nblk = (a.g.n + R - 1) / R;
-    a.nq = a.B / BB;
+    a.nq = a.fused ? a.B : a.B / BB;
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
@@ -914,13 +923,13 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
     const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB>,
+    cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB, FUSED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared memory;
     // the split-unit scratch, the piece counters and kMaxPieces assume grid <= num_sms <= 256)
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB>, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB, FUSED>, kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     if (num_sms > kMaxPieces || num_sms > kPassCounters - 2) return cudaErrorInvalidConfiguration;
@@ -929,7 +938,7 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    e = cudaLaunchKernelEx(&cfg, k_radon_fwd<BB>, a);
+    e = cudaLaunchKernelEx(&cfg, k_radon_fwd<BB, FUSED>, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
@@ -954,8 +963,10 @@ size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
 
 cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, const FwdScratch &scr,
-                             cudaStream_t s, const FwdMc *mc) {
+                             cudaStream_t s, const FwdMc *mc, bool fused) {
+    if (fused && njobs != 2) return cudaErrorInvalidValue;
     FwdArgs a;
+    a.fused = fused ? 1 : 0;
     a.queue = scr.queue;
     a.scratch = scr.part;
     a.mc_part = mc ? mc->part : nullptr;
@@ -964,7 +975,7 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.mc_out = mc ? mc->out : nullptr;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
-    a.njobs = njobs;
+    a.njobs = fused ? 1 : njobs;  // fused: one unit stream, the jobs are the groups' slots
     a.idx = idx;
     a.m = m;
     a.idx_stride = idx_stride;
@@ -972,6 +983,7 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.g = geom_of(plan);
     a.chunks = (plan->n_det + kChunk - 1) / kChunk;
     if (!mc) a.job[0].y = nullptr;
+    if (fused) return launch_bb<2, true>(a, plan->num_sms, s);
     const int bb = fwd_bb(B, idx_stride);
     switch (bb) {
         case 4: return launch_bb<4>(a, plan->num_sms, s);

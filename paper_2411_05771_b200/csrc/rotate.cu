@@ -157,6 +157,30 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
                 if (b0 + b < a.B) job.out[(b0 + b) * nn + (long)r * n + c] = tp[b];
         }
     }
+    if (BB == 1 && a.fuse) {
+        // job-fused layout (one image, its two jobs x1 / x2 as the two slots of a group of
+        // 2): blocks of 16 lines, [block][pixel][line][slot], this job's slot = blockIdx.z
+        constexpr int RF = 16;
+        const long grp = (long)blockIdx.y * a.nblk * n * 32;
+        const int lim = a.nblk * RF, slot = blockIdx.z;
+        if (job.xr)
+            for (int it = threadIdx.x; it < kT * kT; it += kThreads) {
+                const int rl = it % RF, rest = it / RF;
+                const int cc = rest % kT, rr = rest / kT * RF + rl;
+                const int r = r0 + rr, cg = c0 + cc;
+                if (r < lim && cg < n)
+                    job.xr[grp + ((long)(r / RF) * n + cg) * 32 + (r % RF) * 2 + slot] = tile[rr * kRow + cc];
+            }
+        if (job.xc)
+            for (int it = threadIdx.x; it < kT * kT; it += kThreads) {
+                const int cl = it % RF, rest = it / RF;
+                const int rr = rest % kT, cc = rest / kT * RF + cl;
+                const int r = r0 + rr, cg = c0 + cc;
+                if (r < n && cg < lim)
+                    job.xc[grp + ((long)(cg / RF) * n + r) * 32 + (cg % RF) * 2 + slot] = tile[rr * kRow + cc];
+            }
+        return;
+    }
     const long grp = (long)blockIdx.y * a.nblk * n * 32;  // floats per image group per class
     const int lim = a.nblk * R;                            // packed lines (incl. zero padding)
     // each item is one pixel-line slot of BB floats (16 / 8 / 4 bytes); consecutive threads
@@ -313,15 +337,17 @@ size_t pack_floats(const skei_plan *plan, int B, int bb) {
 }
 
 cudaError_t launch_rotate_pack(const skei_plan *plan, const RotPackJob *jobs, int njobs, int B,
-                               int bb, cudaStream_t s, bool pdl) {
+                               int bb, cudaStream_t s, bool pdl, bool fuse) {
+    if (fuse && (bb != 1 || njobs != 2)) return cudaErrorInvalidValue;
     RotPackArgs a;
     a.pdl = pdl ? 1 : 0;
+    a.fuse = fuse ? 1 : 0;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
     a.n = plan->n;
     a.B = B;
     a.rot = plan->d_rot;
-    const int R = 32 / bb;
+    const int R = fuse ? 16 : 32 / bb;  // lines per packed block (fused: 2 slots per line)
     a.nblk = (plan->n + R - 1) / R;
     // tiles cover the image and every packed line (incl. the zero padding lines)
     const int side = a.nblk * R > plan->n ? a.nblk * R : plan->n;
