@@ -83,10 +83,14 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     off += align256(sizeof(float) * adj_ei_part_floats(plan, B));
     w.fscr = off;  // forward split-unit pieces
     off += align256(sizeof(float) * fwd_scratch_floats(plan));
-    w.qi = off;  // interleaved padded q and r for the backprojector's bulk copies
-    off += align256(sizeof(float) * adj_il_floats(plan, B, m));
+    // interleaved padded q and r for the backprojector's bulk copies (job-fused pass: one
+    // buffer of both, spanning qi and ri)
+    size_t il = adj_il_floats(plan, B, m);
+    if ((adj_fused_floats(plan, B, m) + 1) / 2 > il) il = (adj_fused_floats(plan, B, m) + 1) / 2;
+    w.qi = off;
+    off += align256(sizeof(float) * il);
     w.ri = off;
-    off += align256(sizeof(float) * adj_il_floats(plan, B, m));
+    off += align256(sizeof(float) * il);
     w.aux = off;  // skei_sketch_deviation: the full angle list and the fp64 norm partials
     off += align256(sizeof(int32_t) * (size_t)plan->n_full) +
            align256(sizeof(double) * (size_t)B * kNormChunks);
@@ -581,8 +585,10 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     // epilogue, and p2 = A_S x2, in one launch
     // with image groups of 4, q and r are also written in the backprojector's interleaved
     // padded layout (its windows are then one bulk copy per angle)
+    // (job-fused pass: q and r of an image interleaved as the two slots of one row, one buffer)
     const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
-    float *qi = il ? ws_f(ws, wl.qi) : nullptr, *ri = il ? ws_f(ws, wl.ri) : nullptr;
+    float *qi = il || fuse ? ws_f(ws, wl.qi) : nullptr;
+    float *ri = il ? ws_f(ws, wl.ri) : fuse ? qi : nullptr;
     FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[fuse ? 2 : 1]), o->p1, y, o->r, y_sketched},
                     {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
     FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
@@ -598,13 +604,14 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
                                    rei->iter, rei->image0, plan->num_sms, s));
         pin = pn;
     }
-    SKEI_CUDA(launch_ramp(plan, pin, o->q, B * m, s, qi, m, 4, o->r, ri));
+    SKEI_CUDA(launch_ramp(plan, pin, o->q, B * m, s, qi, m, fuse ? 2 : 4, o->r, ri, 1.f, nullptr, fuse));
     SKEI_CUDA(mark(3));
     // a5 + a8 (+ a7 EI part when x3 is the identity network's x_fbp): x_fbp = (pi/2m) A_S^T q
     // and grad = 2 A_S^T r in one launch, ei = ||x2 - x_fbp||^2 fused into its epilogue
     AdjJob aj[2] = {{o->q, o->xfbp, fbp_scale, qi}, {o->r, o->grad, 2.0f, ri}};
     AdjEi eif{o->x2, ws_f(ws, wl.eipart), ctr + 1, o->ei};
-    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, x3_in ? nullptr : &eif));
+    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, s, x3_in ? nullptr : &eif, 0, -1,
+                               fuse));
     SKEI_CUDA(mark(4));
     if (x3_in)  // a7 (EI part) against a caller-provided x3
         SKEI_CUDA(launch_residual(plan, nullptr, nullptr, idx, m, idx_stride, o->x2, x3_in, B,

@@ -113,6 +113,12 @@ constexpr int kAdjPad = 48;
 inline size_t adj_il_floats(const skei_plan *plan, int B, int m) {
     return (size_t)((B + 3) / 4) * m * (plan->n_det + 2 * kAdjPad) * 4;
 }
+// The job-fused pass (one image per group): q and r of image b interleaved as the two slots
+// of one row, [b][k][kAdjPad + j][2], rows of even width (16-byte-aligned even windows)
+inline int adj_fused_wp(const skei_plan *plan) { return (plan->n_det + 2 * kAdjPad + 1) & ~1; }
+inline size_t adj_fused_floats(const skei_plan *plan, int B, int m) {
+    return (size_t)B * m * adj_fused_wp(plan) * 2;
+}
 // pi: the same sinogram as p in the interleaved layout (or NULL: staged from p)
 // base: if set, x = base + scale A^T p (same layout as x)
 struct AdjJob {
@@ -131,9 +137,12 @@ struct AdjEi {
 size_t adj_ei_part_floats(const skei_plan *plan, int B);
 // row0, rows: backproject only output rows [row0, row0 + rows) into [B][rows][n] outputs
 // (rows < 0: whole images)
+// fused: the two jobs are the slots of each image's group (job-fused pass): both jobs' pi
+// point to the fused interleaved q / r rows (adj_fused_floats)
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
-                             const AdjEi *ei = nullptr, int row0 = 0, int rows = -1);
+                             const AdjEi *ei = nullptr, int row0 = 0, int rows = -1,
+                             bool fused = false);
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 // Theorem-1 deviation helpers (deviation.cu): part = [B][kNormChunks] fp64 chunk partials
@@ -158,7 +167,7 @@ struct RampPeers {
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi = nullptr, int m = 0, int bb = 0,
                         const float *rs = nullptr, float *ri = nullptr, float rscale = 1.f,
-                        const RampPeers *peers = nullptr);
+                        const RampPeers *peers = nullptr, bool fused = false);
 
 // Residual: partials in ws (float2 per (image, chunk)), then final reduce.
 size_t residual_ws_bytes(const skei_plan *plan, int B, int m);

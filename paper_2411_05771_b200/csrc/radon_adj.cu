@@ -104,8 +104,11 @@ __device__ __forceinline__ void hat3(float u, float &w0, float &w1, float &w2) {
     w2 = fmaxf(0.f, u - 1.f);
 }
 
-// BULK: every job's windows are bulk copies from its interleaved padded sinogram (BB = 4)
-template <int BB, int NJ, bool BULK>
+// BULK: every job's windows are bulk copies from its interleaved padded sinogram (BB = 4).
+// FUSED (BB = 2, NJ = 1, BULK): one image per CTA, its two jobs (q -> x_fbp, r -> grad) are
+// the group's two slots, staged from the fused interleaved rows [b][k][pad + j][2] (window
+// origins even, so every copy is 16-byte aligned); slot b writes job b's output.
+template <int BB, int NJ, bool BULK, bool FUSED = false>
 __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     __shared__ __align__(128) float win[2][NJ][kKC * kW * BB];
     // per-angle table: entry k of the sketch at [k] when m <= kTab (built once, by all
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
     const int tr0 = a.row0 + (tile / a.tiles_x) * kTileH, tc0 = (tile % a.tiles_x) * kTileW;
-    const int b0 = blockIdx.y * BB;
+    const int b0 = FUSED ? blockIdx.y : blockIdx.y * BB;  // first image (fused: the image)
     const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp w: rows 8*(w/2) .. +7, pixel pairs 8*(w%2) .. +7; lane: row (lane % 8), pairs
@@ -155,7 +158,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         // detector position of the tile origin pixel (tr0, tc0), fp64
         const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
         const double jmin = J0 + fmin(0.0, (kTileW - 1) * cs.x) + fmin(0.0, -(kTileH - 1) * cs.y);
-        const double w0 = floor(jmin);
+        // (fused rows: an even origin, so the 8-byte bins of a window start 16-byte aligned)
+        const double w0 = FUSED ? 2.0 * floor(0.5 * jmin) : floor(jmin);
         s_off[e] = (float)(J0 - w0);
         s_cos[e] = (float)cs.x;
         s_sin[e] = (float)cs.y;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         constexpr unsigned bytes = kW * BB * sizeof(float);
         fence_proxy_async();  // earlier generic reads of this buffer -> async-proxy writes
         mbar_expect_tx(&full[bf], bytes * kc * NJ);
-        const long wp = a.g.n_det + 2 * kAdjPad;
+        const long wp = FUSED ? (long)((a.g.n_det + 2 * kAdjPad + 1) & ~1) : a.g.n_det + 2 * kAdjPad;
         for (int t = 0; t < kc; ++t) {
             const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[tbase(ch) + t];
 #pragma unroll
@@ -286,27 +290,30 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     for (int b = 0; b < BB; ++b) eacc[b] = 0.f;
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj) {
-        const float sc = a.job[jj].scale;
 #pragma unroll
         for (int p = 0; p < kPairs; ++p) {
             const int c = tc0 + 2 * (pc0 + 16 * p);
             if (r >= a.row1) continue;
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
-                const long o = (long)(b0 + b) * nn + (long)r * n + c;  // in a whole image
-                const long ox = (long)(b0 + b) * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
+                // the output of (job jj, image slot b); fused: job b of image b0
+                const AdjJob &jo = a.job[FUSED ? b : jj];
+                const int img = FUSED ? b0 : b0 + b;
+                const float sc = jo.scale;
+                const long o = (long)img * nn + (long)r * n + c;  // in a whole image
+                const long ox = (long)img * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
                 float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
-                if (a.job[jj].base) {  // x = base + scale A^T p
-                    if (c < n) v0 += __ldg(a.job[jj].base + ox);
-                    if (c + 1 < n) v1 += __ldg(a.job[jj].base + ox + 1);
+                if (jo.base) {  // x = base + scale A^T p
+                    if (c < n) v0 += __ldg(jo.base + ox);
+                    if (c + 1 < n) v1 += __ldg(jo.base + ox + 1);
                 }
                 if (c + 1 < n && ((ox & 1) == 0)) {
-                    *reinterpret_cast<float2 *>(a.job[jj].x + ox) = make_float2(v0, v1);
+                    *reinterpret_cast<float2 *>(jo.x + ox) = make_float2(v0, v1);
                 } else {
-                    if (c < n) a.job[jj].x[ox] = v0;
-                    if (c + 1 < n) a.job[jj].x[ox + 1] = v1;
+                    if (c < n) jo.x[ox] = v0;
+                    if (c + 1 < n) jo.x[ox + 1] = v1;
                 }
-                if (jj == 0 && a.ei_x2) {
+                if (jj == 0 && (!FUSED || b == 0) && a.ei_x2) {
                     if (c < n) {
                         const float d = __ldg(a.ei_x2 + o) - v0;
                         eacc[b] = fmaf(d, d, eacc[b]);
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     }
     __syncthreads();
     const int ntiles = gridDim.x;
-    if (threadIdx.x < BB) {
+    if (threadIdx.x < (FUSED ? 1 : BB)) {
         float v = 0.f;
         for (int w = 0; w < kThreads / 32; ++w) v += s_red[w][threadIdx.x];
         a.ei_part[(long)(b0 + threadIdx.x) * ntiles + tile] = v;
@@ -353,6 +360,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         if (lane == 0) a.ei_out[b] = (float)s;
     }
     if (threadIdx.x == 0) *a.ei_ctr = 0u;  // ready for the next launch
+}
+
+cudaError_t launch_fused(const AdjArgs &a, int B, cudaStream_t s) {
+    dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)B, 1);
+    k_radon_adj<2, 1, true, true><<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <int BB>
@@ -384,7 +397,8 @@ size_t adj_ei_part_floats(const skei_plan *plan, int B) {
 
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
-                             const AdjEi *ei, int row0, int rows) {
+                             const AdjEi *ei, int row0, int rows, bool fused) {
+    if (fused && (njobs != 2 || !jobs[0].pi)) return cudaErrorInvalidValue;
     AdjArgs a;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
@@ -401,6 +415,7 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
     a.ei_part = ei ? ei->part : nullptr;
     a.ei_ctr = ei ? ei->ctr : nullptr;
     a.ei_out = ei ? ei->out : nullptr;
+    if (fused) return launch_fused(a, B, s);
     const int bb = pick_bb(B, idx_stride);
     switch (bb) {
         case 4: return launch_bb<4>(a, njobs, B, s);

@@ -95,6 +95,10 @@ struct RampArgs {
     // both sides (rows of width wp = n_det + 2 kAdjPad)
     float *qi;
     int m, bb, wp;
+    // fused (the job-fused pass, one image per group): q and r of image b are the two slots of
+    // one interleaved row, qi[b][k][kAdjPad + j][slot] (slot 0 = q, 1 = r), rows of even width
+    // wp so that every 16-byte-aligned window start is an even bin
+    int fused;
     // optional: CTAs nramp.. copy the residual r [B][m][n_det] into the same interleaved
     // layout (one CTA per (image group of 4, angle): 16-byte stores)
     const float *rs;
@@ -110,6 +114,7 @@ struct RampArgs {
 };
 __device__ __forceinline__ float *il_row(const RampArgs &a, int row) {
     const int b = row / a.m, k = row - b * a.m;
+    if (a.fused) return a.qi + ((long)row * a.wp + kAdjPad) * 2;  // slot 0 of row (b, k)
     return a.qi + ((long)((b / a.bb) * a.m + k) * a.wp + kAdjPad) * a.bb + b % a.bb;
 }
 
@@ -209,6 +214,16 @@ __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
         }
         return;
     }
+    if ((int)blockIdx.x >= a.nramp && a.fused) {  // r row u into slot 1 of the fused rows
+        const int u = blockIdx.x - a.nramp;
+        const float *src = a.rs + (long)u * a.n_det;
+        float *dst = a.ri + (long)u * a.wp * 2 + 1;
+        for (int o = threadIdx.x; o < a.wp; o += blockDim.x) {
+            const int j = o - kAdjPad;
+            dst[(long)o * 2] = (j >= 0 && j < a.n_det) ? __ldg(src + j) : 0.f;
+        }
+        return;
+    }
     if ((int)blockIdx.x >= a.nramp) {  // interleave r: group g = u / m of 4 images, angle k
         const int u = blockIdx.x - a.nramp, g = u / a.m, k = u - g * a.m;
         const long stride = (long)a.m * a.n_det;  // between images
@@ -250,8 +265,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
         SKEI_PASS(RL, kOut, true, last);
     }
 #undef SKEI_PASS
-    if (ia) {  // the zero pads of the interleaved rows
-        for (int t = threadIdx.x; t < 2 * kAdjPad; t += blockDim.x) {
+    if (ia) {  // the zero pads of the interleaved rows (fused rows: up to the even width)
+        const int npad = a.wp - a.n_det;
+        for (int t = threadIdx.x; t < npad; t += blockDim.x) {
             const int o = t < kAdjPad ? t - kAdjPad : a.n_det + (t - kAdjPad);
             ia[(long)o * a.bb] = 0.f;
             if (ib) ib[(long)o * a.bb] = 0.f;
@@ -288,8 +304,9 @@ void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal) 
 
 cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int rows,
                         cudaStream_t s, float *qi, int m, int bb, const float *rs, float *ri,
-                        float rscale, const RampPeers *peers) {
+                        float rscale, const RampPeers *peers, bool fused) {
     RampArgs a;
+    a.fused = fused ? 1 : 0;
     a.npeer = peers ? peers->n : 0;
     for (int g = 0; g < kMaxPeers; ++g) {
         a.pq[g] = peers && g < peers->n ? peers->q[g] : nullptr;
@@ -303,7 +320,8 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     a.qi = qi;
     a.m = m > 0 ? m : 1;
     a.bb = bb > 0 ? bb : 1;
-    a.wp = plan->n_det + 2 * kAdjPad;
+    a.wp = fused ? adj_fused_wp(plan) : plan->n_det + 2 * kAdjPad;
+    if (fused) a.bb = 2;
     a.p = p;
     a.q = q;
     a.rows = rows;
@@ -320,7 +338,8 @@ cudaError_t launch_ramp(const skei_plan *plan, const float *p, float *q, int row
     // + the interleaving CTAs of r (rows / m images in groups of 4, m angles each), or with
     // peers the CTAs that copy each local r row to the peers
     const bool pe = peers && peers->n > 0;
-    const int grid = a.nramp + (pe ? (rs ? rows : 0) : (ri && rs ? (rows / a.m / 4) * a.m : 0));
+    const int grid = a.nramp + (pe ? (rs ? rows : 0)
+                                   : (ri && rs ? (fused ? rows : (rows / a.m / 4) * a.m) : 0));
     cudaError_t e = cudaSuccess;
 #define SKEI_RAMP_LAUNCH4(RLV, MT, MB, PE)                                                      \
     do {                                                                                        \
