@@ -27,13 +27,20 @@
  *                    the device).
  *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
  *     default stream), performs no device allocation and no hidden sync, and is
- *     deterministic: no atomics, fixed reduction order, bitwise-repeatable.
+ *     deterministic: no floating-point atomics, fixed reduction order, bitwise-
+ *     repeatable.  The only atomics are integer completion counters (atomicAdd on
+ *     unsigned words in the workspace) that elect which CTA performs a fixed-order
+ *     final sum; the counters reset themselves before the kernel exits.
  *   - Arguments are validated on the host before any launch; a failing check
  *     returns SKEI_ERR_SHAPE / SKEI_ERR_CONFIG / SKEI_ERR_ARG and launches nothing.
  *     A launch failure returns SKEI_ERR_CUDA; asynchronous faults surface at the
  *     caller's next synchronisation.
  *   - A plan is immutable after creation and may be used from several streams and
- *     threads concurrently (it owns only read-only device tables).
+ *     threads concurrently (it owns only read-only device tables).  A workspace `ws`
+ *     may NOT be shared by calls that can run concurrently (two streams, or two
+ *     threads' calls on one stream that may interleave): it holds the packed images,
+ *     the filtered sinogram and the self-resetting completion counters of the call in
+ *     flight.  Calls on one stream may reuse one workspace back to back.
  */
 #ifndef SKEI_H
 #define SKEI_H
@@ -132,17 +139,6 @@ skei_status skei_rotate(const skei_plan *plan, const float *x, float *out, int32
 skei_status skei_rotate_adjoint(const skei_plan *plan, const float *y, float *out, int32_t B,
                                 const int32_t *g_deg, int32_t g_stride, skei_stream stream);
 
-/* ------------------------- next row (SURVEY §8(f) #1): the EI branch's gradient --
- * grad = d ||x2 - x3||^2 / d x1 for x2 = T_g x1 and the identity network
- * x3 = M x2, M = (pi/2m) A_S^T ramp A_S (the sketched FBP, R16; PAPER.md Eq. 6
- * L97-L101, Alg. 1 steps 4-6 L120-L122).  M is symmetric, so
- *   grad = T_g^T (I - M) d,   d = 2 (x2 - x3),
- * computed as: d (packed for the projector), A_S d, ramp, u = d - (pi/2m) A_S^T q,
- * T_g^T u — five launches on `stream`.  x2, x3: [B][n][n] device (skei_pass's x2 and
- * xfbp); g_deg, g_stride as skei_rotate; idx, m, idx_stride as skei_radon_fwd;
- * grad: [B][n][n] device, must not alias x2 or x3; ws >= skei_workspace_bytes(plan, B, m).
- * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL, strides,
- * aliasing, ws too small). */
 /* ---------------- next row: communication-reduced single-image split --
  * The backprojections of the pass restricted to output rows [row0, row0 + rows): with q
  * (the filtered sinogram) and r (the residual) of ALL m sketched angles at hand — after
@@ -196,6 +192,17 @@ skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, in
                              const int32_t *idx, int32_t m, int32_t idx_stride, int32_t m_total,
                              void *ws, size_t ws_bytes, skei_stream stream);
 
+/* ------------------------- next row (SURVEY §8(f) #1): the EI branch's gradient --
+ * grad = d ||x2 - x3||^2 / d x1 for x2 = T_g x1 and the identity network
+ * x3 = M x2, M = (pi/2m) A_S^T ramp A_S (the sketched FBP, R16; PAPER.md Eq. 6
+ * L97-L101, Alg. 1 steps 4-6 L120-L122).  M is symmetric, so
+ *   grad = T_g^T (I - M) d,   d = 2 (x2 - x3),
+ * computed as: d (packed for the projector), A_S d, ramp, u = d - (pi/2m) A_S^T q,
+ * T_g^T u — five launches on `stream`.  x2, x3: [B][n][n] device (skei_pass's x2 and
+ * xfbp); g_deg, g_stride as skei_rotate; idx, m, idx_stride as skei_radon_fwd;
+ * grad: [B][n][n] device, must not alias x2 or x3; ws >= skei_workspace_bytes(plan, B, m).
+ * Errors: SKEI_ERR_SHAPE (B < 1, m < 1 or m > n_full), SKEI_ERR_ARG (NULL, strides,
+ * aliasing, ws too small). */
 skei_status skei_ei_grad(const skei_plan *plan, int32_t B, const float *x2, const float *x3,
                          const int32_t *g_deg, int32_t g_stride, const int32_t *idx, int32_t m,
                          int32_t idx_stride, float *grad, void *ws, size_t ws_bytes,
@@ -349,6 +356,17 @@ skei_status skei_pass_draw(const skei_plan *plan, int32_t B, const float *x1, co
  * floats) receives per-block checksums so the loads cannot be elided.  Bytes read =
  * blocks * 1024 * 16 * 32 * iters. */
 skei_status skei_smem_probe(float *sink, int32_t blocks, int32_t iters, skei_stream stream);
+
+/* Diagnostic: L2 read bandwidth probe (the bound of the forward
+ * projector's re-staging of packed line blocks, which after the first unit come from L2).
+ * `blocks` CTAs of 1024 threads each read the whole device buffer buf[n_floats] `iters`
+ * times with L1-bypassing 16-byte loads (each CTA from its own starting offset); size buf
+ * well under the L2 (cudaDevAttrL2CacheSize) so the sweeps after the first hit L2.
+ * sink: device, >= blocks floats (checksums).  Bytes read = blocks * n_floats * 4 * iters.
+ * Errors: SKEI_ERR_ARG (NULL, blocks / iters < 1, n_floats < 4096 or not a multiple of 4,
+ * buf not 16-byte aligned). */
+skei_status skei_l2_probe(const float *buf, int64_t n_floats, float *sink, int32_t blocks,
+                          int32_t iters, skei_stream stream);
 
 /* Library build info: "skei <version> sm_100a". */
 const char *skei_version(void);

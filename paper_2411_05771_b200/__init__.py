@@ -27,7 +27,7 @@ import torch
 __all__ = [
     "Plan", "SkeiError", "lib", "lib_path", "draw", "draw_device", "rotate", "radon_fwd",
     "radon_adj", "ramp_filter", "fbp", "ei_residual", "sketched_pass", "sketched_pass_host",
-    "sketched_pass_profiled", "sketched_pass_draw", "smem_probe", "alloc_pass_outputs",
+    "sketched_pass_profiled", "sketched_pass_draw", "smem_probe", "l2_probe", "alloc_pass_outputs",
     "workspace_bytes", "MODE_INTERLEAVED", "MODE_UNIFORM", "SHARED_IMAGE", "version",
 ]
 
@@ -104,6 +104,7 @@ def lib():
             "skei_pass_draw": ([vp, i32, vp, vp, ctypes.POINTER(_DrawSpec), i32, vp, vp,
                                 ctypes.POINTER(_PassOut), vp, sz, ctypes.POINTER(vp), i32, vp], st),
             "skei_smem_probe": ([vp, i32, i32, vp], st),
+            "skei_l2_probe": ([vp, ctypes.c_int64, vp, i32, i32, vp], st),
             "skei_version": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -481,6 +482,12 @@ def sketched_pass_draw(plan: Plan, x1, y, seed: int, it: int, m: int, mode: int 
                                 _ptr(ws, torch.uint8, "ws"), ws.numel(), ev, nev, _stream(x1)),
            "skei_pass_draw")
     return out, g, idx
+
+
+def l2_probe(buf: torch.Tensor, blocks: int, iters: int, sink: torch.Tensor):
+    """skei_l2_probe (diagnostic): L2 read bandwidth; bytes = blocks*buf.numel()*4*iters."""
+    _check(lib().skei_l2_probe(_ptr(buf, name="buf"), buf.numel(), _ptr(sink, name="sink"), blocks,
+                               iters, _stream(sink)), "skei_l2_probe")
 
 
 def smem_probe(blocks: int, iters: int, sink: torch.Tensor):

@@ -675,6 +675,15 @@ skei_status skei_smem_probe(float *sink, int32_t blocks, int32_t iters, skei_str
     return SKEI_OK;
 }
 
+skei_status skei_l2_probe(const float *buf, int64_t n_floats, float *sink, int32_t blocks,
+                          int32_t iters, skei_stream stream) {
+    if (!buf || !sink || blocks < 1 || iters < 1 || n_floats < 4 * 1024 || n_floats % 4)
+        return SKEI_ERR_ARG;
+    if (((uintptr_t)buf & 15) != 0) return SKEI_ERR_ARG;
+    SKEI_CUDA(launch_l2_probe(buf, (long)n_floats, sink, blocks, iters, (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
 skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
                            const float *h_y, const int32_t *h_g, int32_t g_stride,
                            const int32_t *h_idx, int32_t m, int32_t idx_stride, float *d_x1,
@@ -687,13 +696,18 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
     skei_status st = check_idx_args(plan, B, h_idx, m, idx_stride);
     if (st != SKEI_OK) return st;
     if (g_stride != 0 && g_stride != 1) return SKEI_ERR_ARG;
+    // everything run_pass would reject is rejected here, before the first copy
+    if (!ws || ws_bytes < skei_workspace_bytes(plan, B, m)) return SKEI_ERR_ARG;
+    if (!o->x2 || !o->p1 || !o->p2 || !o->q || !o->xfbp || !o->r || !o->grad || !o->mc ||
+        !o->ei)
+        return SKEI_ERR_ARG;
+    for (long i = 0; i < (long)m * (idx_stride ? B : 1); ++i)  // host indices: checked here
+        if (h_idx[i] < 0 || h_idx[i] >= plan->n_full) return SKEI_ERR_ARG;
     DeviceGuard guard(plan->device);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t nn = (size_t)plan->n * plan->n, ny = (size_t)plan->n_full * plan->n_det;
     SKEI_CUDA(cudaMemcpyAsync(d_x1, h_x1, sizeof(float) * B * nn, cudaMemcpyHostToDevice, s));
     const int n_det = plan->n_det;
-    for (long i = 0; i < (long)m * (idx_stride ? B : 1); ++i)  // host indices: checked here
-        if (h_idx[i] < 0 || h_idx[i] >= plan->n_full) return SKEI_ERR_ARG;
     // With one sketch for the batch only the m sketched rows of y cross the link: each run
     // of consecutive angle indices is one strided copy of B row blocks, into d_y as y_S
     // [B][m][n_det] (the pass then reads y_S row k for angle idx[k]).  Per-image sketches

@@ -180,6 +180,8 @@ cudaError_t launch_draw(uint64_t seed, uint64_t iter, uint64_t image0, int count
                         int n_full, int m, int mode, int32_t *g, int32_t *idx, cudaStream_t s);
 
 cudaError_t launch_smem_probe(float *sink, int blocks, int iters, cudaStream_t s);
+cudaError_t launch_l2_probe(const float *buf, long n_floats, float *sink, int blocks, int iters,
+                            cudaStream_t s);
 
 // Host draw (library implementation of DESIGN.md R5).
 int host_draw(uint64_t seed, uint64_t iter, uint64_t image, int n_full, int m, int mode,
