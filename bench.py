@@ -720,6 +720,16 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     probe_gbs = 2 * nsm * 1024 * 16 * 32 * 1000 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    # L2 read bandwidth probe: the forward re-stages its packed line blocks from
+    # L2, so this bounds its TMA traffic (a 32 MB buffer, well under the 126 MB L2)
+    l2buf = torch.ones(8 << 20, device=dev)
+    sk.l2_probe(l2buf, nsm, 2, sink)
+    e0.record()
+    sk.l2_probe(l2buf, nsm, 10, sink)
+    e1.record()
+    torch.cuda.synchronize()
+    l2_gbs = nsm * l2buf.numel() * 4 * 10 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del l2buf
 
     if world > 1:
         dist.barrier()
@@ -873,6 +883,7 @@ def main():
         "algorithmic": f"4 B per tap, {taps[dname]:.4g} taps per launch "
                        f"(2 jobs x {B} images x {m} angles x {N}^2 px x 2 taps)",
         "kernel_ms": float(fwd_ms.mean()),
+        "l2_probe_gbs": l2_gbs,
         "pass_frac": pass_frac,
         "pass_roofline": f"max(T_gather = 4 B x {taps_per_pass(lcfg):.4g} taps / peak, T_hbm = "
                          f"{hbm_bytes_per_pass(lcfg):.4g} B / {hbm_gbs:g} GB/s ({hbm_src})) / "

@@ -4,6 +4,27 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
+
+// Device-side invariant checks of the checked build (nvcc -DSKEI_CHECKS, e.g.
+// `python tools/build_variant.py ab/libskei_checked.so -DSKEI_CHECKS`, then SKEI_LIB=... for the
+// tests): the sanitizer substitute on this pool, where compute-sanitizer is closed.  A failed
+// check prints its site and traps (the launch then fails with an illegal-instruction error).
+// Compiled out of the product build.
+#ifdef SKEI_CHECKS
+#define SKEI_DCHECK(cond, what)                                                              \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("SKEI_DCHECK failed: %s at %s:%d (block %d,%d thread %d)\n", what, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);            \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define SKEI_DCHECK(cond, what) \
+    do {                        \
+    } while (0)
+#endif
 
 #include "../../include/skei.h"
 

@@ -189,6 +189,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
         const long wp = FUSED ? (long)((a.g.n_det + 2 * kAdjPad + 1) & ~1) : a.g.n_det + 2 * kAdjPad;
         for (int t = 0; t < kc; ++t) {
             const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[tbase(ch) + t];
+            SKEI_DCHECK(s_w0[tbase(ch) + t] >= -kAdjPad &&
+                            kAdjPad + s_w0[tbase(ch) + t] + kW <= wp,
+                        "backprojector window inside the padded row");
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj)
                 bulk_g2s(&win[bf][jj][t * kW * BB], a.job[jj].pi + row * BB, bytes, &full[bf]);

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k_ramp(RampArgs a) {
     // global row of local row `row` in the peers' [B][m_total][n_det] buffers
     auto peer_off = [&](int row) -> long {
         const int b = row / a.m_local, k = row - b * a.m_local;
+        SKEI_DCHECK(a.row0 + k < a.m_total && a.row0 >= 0, "ramp peer row");
         return ((long)b * a.m_total + a.row0 + k) * a.n_det;
     };
     if (PEERS && (int)blockIdx.x >= a.nramp) {  // copy local r row u to every peer

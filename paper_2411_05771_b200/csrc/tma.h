@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 
+#include "internal.h"
+
 namespace skei {
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -23,12 +25,34 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
                  : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    // cp.async.bulk: 16-byte aligned addresses, size a non-zero multiple of 16
+    SKEI_DCHECK(((smem_u32(dst) | (unsigned)(uintptr_t)src | bytes) & 15u) == 0u && bytes != 0u,
+                "bulk copy alignment");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
             "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+#ifdef SKEI_CHECKS
+    // checked build: a phase that never completes (a lost or mis-sized copy, a missing
+    // arrive) traps after ~4 s instead of hanging the GPU
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+        if (ok) return;
+        SKEI_DCHECK(clock64() - t0 < 8000000000LL, "mbarrier wait timed out");
+    }
+#else
     // try_wait with a suspend-time hint: a waiting warp sleeps in hardware until the phase
     // completes (or the hint expires) instead of spinning on issue slots other warps need
     asm volatile(
@@ -40,6 +64,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(1000000u)
         : "memory");
+#endif
 }
 
 }  // namespace skei

@@ -79,3 +79,22 @@ def test_reference_arm_steps_fit_its_run_time():
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
     assert d["steps"] * d["ms_per_step"] * 1e-3 <= wall
     assert "whole" in d["cpu_baseline"]["sample"] and d["cpu_baseline"]["host_cores"] >= 1
+
+
+def test_link_probe_two_ranks_gloo():
+    """tools/link_probe.py (SURVEY M2 interconnect probes) under torch.distributed.run with two
+    gloo ranks: rank 0 alone prints one JSON line with the all-reduce, all-gather and
+    point-to-point entries (the numbers are meaningless on CPU)."""
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                          "29547", os.path.join(ROOT, "tools", "link_probe.py"), "--iters", "1",
+                          "--backend", "gloo", "--bytes", "65536"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=_clean_env({}))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["world"] == 2 and d["backend"] == "gloo"
+    assert {"allreduce_65536B", "allgather_2967552B", "p2p_64MB_0to1"} <= set(d)
+    assert all(v["s"] > 0 for k, v in d.items() if isinstance(v, dict))
