@@ -47,6 +47,7 @@
 //     to finish (completion counter).  A split unit's pieces go to L2 slots and the last
 //     piece to arrive adds them in CTA order (deterministic, no float atomics).
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 #include "tma.h"
@@ -78,6 +79,9 @@ constexpr int kKMax = 16;   // angles per CTA
 #define SKEI_FWD_AHEAD 1
 #endif
 constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ahead of use
+#ifndef SKEI_FWD_WIDE_SPLIT
+#define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
+#endif
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
 constexpr int kCand = 5;    // candidate pixels of a bin pair per line
 constexpr int kPadL = 5;    // zero pixel columns left of the line data (candidates from -5)
@@ -239,6 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     const int stage_f = (n + kPadL + kPadR) * kColF;
     int4 *btab = reinterpret_cast<int4 *>(smem + a.nbuf * stage_f);  // [K][nb] block table
     const long part_f = (long)K * n_det * BB;
+    SKEI_DCHECK(part_f <= (long)kWarps * kMaxTaskBB * kChunk && ncl <= kMaxPieces && K <= kKMax &&
+                    nq <= kMaxQ,
+                "forward scratch / piece / table sizes");
 
     // ---- 1. class sizes per image group -> unit table (identical in every CTA)
     for (int q = warp; q < nq; q += kWarps) {
@@ -319,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             if (g < hi - lo) {
                 const UnitId d = decode_unit(U, nq, K, u);
                 const FwdJob &jb = d.job ? a.job[1] : a.job[0];
+                SKEI_DCHECK(d.q < nq && lo + g < a.nblk && d.job < a.njobs, "forward block source");
                 return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + lo + g) * n * kColF;
             }
             g -= hi - lo;
@@ -420,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         // per (angle, block): the block's first-line position of bin 0, A = P0 + lb Pl, split
         // into (int base, fp32 frac) in fp64, and the exact range [jlo, jhi] of bins whose
         // candidates can fall inside the image for some line of the block
+        SKEI_DCHECK(kcnt * nbu <= K * a.nblk && kcnt * a.chunks <= kWarps * kMaxT, "forward unit tables");
         for (int e = threadIdx.x; e < kcnt * nbu; e += kThreads) {
             const int k = e / nbu, i = e - k * nbu;
             const double Pl = sPl[k], Pj = sPj[k];
@@ -537,6 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 float lo[BB], hi[BB];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) lo[b] = hi[b] = 0.f;
+                // the line loop, compiled twice: with and without the fifth candidate (wide is
+                // warp-uniform — a property of the task's angle — so the branch between the two
+                // never diverges, and the ~92% of angles with 4|b| - 1 >= 2 issue no c4 code)
+                auto run_lines = [&](auto wide_tag) {
+                constexpr bool kWide = decltype(wide_tag)::value;
                 // one line: e = a*_lo - 1/|beta| relative to base (a*_lo: the line position
                 // that projects onto the lower bin's centre, the upper one's is a*_lo + 1/|b|).
                 // Candidates c_k = floor(e) + 1 + k, k = 0..4, lie at detector offsets
@@ -562,11 +576,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                         min((unsigned)(base6 + __float_as_int(fl2 + 12582912.f)), cmax);
                     const unsigned pa = (pbase ^ (unsigned)(gc * BB * sizeof(float))) +
                                         cu * (unsigned)(kColF * sizeof(float));
+                    SKEI_DCHECK(pa >= cur_b && pa + (kCand - 1) * kColF * sizeof(float) + BB * sizeof(float) <=
+                                    cur_b + (unsigned)(stage_f * sizeof(float)),
+                                "forward candidate address");
                     lds_px<BB>(pa, vv[0]);
                     lds_px<BB>(pa + kColF * sizeof(float), vv[1]);
                     lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
                     if (fmaf(-ab, phi, off.z) < 1.f) lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
-                    if (wide) {
+                    if constexpr (kWide) {
                         if (fmaf(-ab, phi, off.w) < 1.f)
                             lds_px<BB>(pa + 4 * kColF * sizeof(float), vv[4]);
                     }
@@ -585,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     fma_px<BB>(lo, w2, vv[2]);
                     fma_px<BB>(hi, u2, vv[2]);
                     fma_px<BB>(hi, u3, vv[3]);
-                    if (wide) {
+                    if constexpr (kWide) {
                         const float u4 = fmaxf(1.f - fmaf(-ab, phi, off.w), 0.f);
                         fma_px<BB>(hi, u4, vv[4]);
                     }
@@ -605,7 +622,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #pragma unroll
                 for (int q2 = 0; q2 <= D; ++q2)
 #pragma unroll
-                    for (int b = 0; b < BB; ++b) v[q2][3][b] = v[q2][4][b] = 0.f;
+                    for (int b = 0; b < BB; ++b) {
+                        v[q2][3][b] = 0.f;
+                        if constexpr (kWide) v[q2][4][b] = 0.f;
+                    }
 #pragma unroll
                 for (int st = 0; st < D; ++st) {
                     if (st > 0) advance(st);
@@ -620,6 +640,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     }
                     use_line(v[cur], ph[cur]);
                 }
+                };
+#if SKEI_FWD_WIDE_SPLIT
+                if (wide)
+                    run_lines(std::true_type{});
+                else
+                    run_lines(std::false_type{});
+#else
+                run_lines(std::true_type{});
+#endif
                 if constexpr (kUnrollT) {
 #pragma unroll
                     for (int b = 0; b < BB; ++b) {
@@ -745,6 +774,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 for (int c = c0; c <= c1; ++c) {
                     const long ws = wstart(c);
                     if (wstart(c + 1) == ws) continue;
+                    SKEI_DCHECK(npc < kMaxPieces, "forward pieces per split unit");
                     s_dpiece[di][npc++] = c * 2 + (u == (int)(ws / nbc) ? 0 : 1);
                 }
                 const bool last = atomicAdd(a.queue + c0, 1u) == (unsigned)(npc - 1);
@@ -768,6 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         if (mc && finish && threadIdx.x < (FUSED ? 1 : BB)) {
             float v = 0.f;
             for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
+            SKEI_DCHECK(u - U.uoff[d.q] < a.mc_slots, "forward MC partial slot");
             a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
         }
 #ifdef SKEI_FWD_STATS
@@ -874,7 +905,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             if (threadIdx.x < (FUSED ? 1 : BB)) {
                 float v = 0.f;
                 for (int w = 0; w < kWarps; ++w) v += s_red[w][threadIdx.x];
-                a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
+                SKEI_DCHECK(u - U.uoff[d.q] < a.mc_slots, "forward MC partial slot");
+            a.mc_part[(long)(b0 + threadIdx.x) * a.mc_slots + (u - U.uoff[d.q])] = v;
             }
         }
     }
