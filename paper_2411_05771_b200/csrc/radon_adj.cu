@@ -24,6 +24,8 @@
 //   * Optional fused epilogue (skei_pass with the identity network): ei partial sums
 //     sum (x2 - x_fbp)^2 per tile and image, reduced in fixed order by the last CTA.
 // Work per (pixel, angle, image) = 2 taps; per pixel pair and angle 3 LDS.BB per job.
+#include <type_traits>
+
 #include "internal.h"
 #include "tma.h"
 
@@ -365,7 +367,297 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
     if (threadIdx.x == 0) *a.ei_ctr = 0u;  // ready for the next launch
 }
 
+// ---- quad variant (bulk staging only): each thread owns FOUR horizontally adjacent pixels
+// of one row.  Their positions t_k = t_0 + k cos(th) span 3 |cos th| <= 3 bins, so the quad
+// reads one 5-bin window per (angle, job) — 5 LDS for 4 pixels instead of 6 for two pairs.
+// Pixel i in "canonical" order (i = 0 the pixel with the lowest position: k = i for
+// cos >= 0, k = 3 - i for cos < 0) lies at u_i = u + i |cos| from the window origin
+// (u in [0, 1)), so its 3 candidate bins start at a per-angle offset o_i with
+// o_i in [i |cos| - 1, i |cos|]: o = (0,0,0,0) for |cos| <= 1/3, (0,0,0,1) for <= 1/2,
+// (0,0,1,1) for <= 2/3, else (0,0,1,2) — warp-uniform, so each (pattern, sign) is its own
+// compiled body (static register indexing).  The lanes of a quarter-warp are 8 consecutive
+// rows of one quad column (conflict-free, as the pair kernel).  Tile 32 x 32, 256 threads.
+constexpr int kQTileH = 32;  // quad tile height (rows); width kTileW
+constexpr int kQW = 48;      // staged bins per angle (>= 31 sqrt 2 + 4)
+constexpr int kQKC = 12;     // angles per staged chunk
+#ifndef SKEI_ADJQ_MINB
+#define SKEI_ADJQ_MINB 3     // CTAs per SM the quad kernel is compiled for
+#endif
+#ifndef SKEI_ADJQ_UNROLL
+#define SKEI_ADJQ_UNROLL 1   // angles unrolled in the quad kernel's loop
+#endif
+constexpr int kQUnroll = SKEI_ADJQ_UNROLL;
+
+template <int BB, int NJ, bool BULK, bool FUSED>
+__global__ void __launch_bounds__(kThreads, SKEI_ADJQ_MINB) k_radon_adj_quad(AdjArgs a) {
+    __shared__ __align__(128) float win[2][NJ][kQKC * kQW * BB];
+    __shared__ float s_off[kTab], s_cos[kTab], s_sin[kTab];
+    __shared__ int s_w0[kTab], s_pat[kTab];
+    __shared__ float s_red[kThreads / 32][BB];
+    __shared__ bool s_last;
+    __shared__ __align__(8) uint64_t full[2];
+
+    const int n = a.g.n, n_det = a.g.n_det;
+    const int tile = blockIdx.x;
+    const int tr0 = a.row0 + (tile / a.tiles_x) * kQTileH, tc0 = (tile % a.tiles_x) * kTileW;
+    const int b0 = FUSED ? blockIdx.y : blockIdx.y * BB;
+    const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp w: rows 8 (w & 3) .. +7, quad columns 4 (w >> 2) .. +3; a quarter-warp = 8 rows
+    const int ry = 8 * (warp & 3) + (lane & 7);
+    const int qc = 4 * (warp >> 2) + (lane >> 3);  // quad index 0..7
+    const long nn = (long)n * n;
+
+    float acc[NJ][4][BB];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < BB; ++b) acc[j][q][b] = 0.f;
+
+    const int nchunks = (a.m + kQKC - 1) / kQKC;
+    if (BULK && threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+    }
+    const bool full_tab = a.m <= kTab;
+    auto entry = [&](int k, int e) {
+        const double2 cs = a.g.trig[idx[k]];
+        const double J0 = a.g.hd + (tc0 - a.g.h) * cs.x + (a.g.h - tr0) * cs.y;
+        const double jmin = J0 + fmin(0.0, (kTileW - 1) * cs.x) + fmin(0.0, -(kQTileH - 1) * cs.y);
+        const double w0 = FUSED ? 2.0 * floor(0.5 * jmin) : floor(jmin);
+        s_off[e] = (float)(J0 - w0);
+        const float cf = (float)cs.x, ac = fabsf(cf);
+        s_cos[e] = cf;
+        s_sin[e] = (float)cs.y;
+        s_w0[e] = (int)w0;
+        const int pat = ac <= (1.f / 3.f) ? 0 : ac <= 0.5f ? 1 : ac <= (2.f / 3.f) ? 2 : 3;
+        s_pat[e] = pat | (cf < 0.f ? 4 : 0);
+    };
+    auto tbase = [&](int ch) { return full_tab ? ch * kQKC : (ch & 1) * kQKC; };
+    auto table = [&](int ch) {
+        const int k0 = ch * kQKC;
+        const int kc = min(kQKC, a.m - k0);
+        if (!full_tab && threadIdx.x < kc) entry(k0 + threadIdx.x, tbase(ch) + threadIdx.x);
+    };
+    if (full_tab)
+        for (int k = threadIdx.x; k < a.m; k += kThreads) entry(k, k);
+    __syncthreads();
+    auto issue_bulk = [&](int ch, int bf) {
+        const int k0 = ch * kQKC;
+        const int kc = min(kQKC, a.m - k0);
+        constexpr unsigned bytes = kQW * BB * sizeof(float);
+        fence_proxy_async();
+        mbar_expect_tx(&full[bf], bytes * kc * NJ);
+        const long wp = FUSED ? (long)((a.g.n_det + 2 * kAdjPad + 1) & ~1) : a.g.n_det + 2 * kAdjPad;
+        for (int t = 0; t < kc; ++t) {
+            const long row = ((long)blockIdx.y * a.m + k0 + t) * wp + kAdjPad + s_w0[tbase(ch) + t];
+            SKEI_DCHECK(s_w0[tbase(ch) + t] >= -kAdjPad && kAdjPad + s_w0[tbase(ch) + t] + kQW <= wp,
+                        "quad backprojector window inside the padded row");
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj)
+                bulk_g2s(&win[bf][jj][t * kQW * BB], a.job[jj].pi + row * BB, bytes, &full[bf]);
+        }
+    };
+    auto produce = [&](int ch, int bf) {
+        if (warp == 0) {
+            table(ch);
+            __syncwarp();
+            if (lane == 0) issue_bulk(ch, bf);
+        }
+    };
+    // plain path (standalone calls: all threads): table, then element-wise cp.async from the
+    // plain sinograms, zero outside [0, n_det) — the same window contents as the bulk copies
+    auto stage = [&](int ch, int bf) {
+        const int k0 = ch * kQKC;
+        const int kc = min(kQKC, a.m - k0);
+        table(ch);
+        __syncthreads();  // window origins visible
+        for (int e = threadIdx.x; e < kc * kQW * BB; e += kThreads) {
+            const int b = e % BB;
+            const int w = (e / BB) % kQW;
+            const int t = e / (BB * kQW);
+            const int jb = s_w0[tbase(ch) + t] + w;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                float *dst = &win[bf][jj][e];
+                if (jb >= 0 && jb < n_det)
+                    cp_async4(dst, a.job[jj].p + ((long)(b0 + b) * a.m + k0 + t) * n_det + jb);
+                else
+                    *dst = 0.f;
+            }
+        }
+        cp_async_commit();
+    };
+    if constexpr (BULK) {
+        produce(0, 0);
+        if (nchunks > 1) produce(1, 1);
+    } else {
+        stage(0, 0);
+    }
+
+    // one angle: the quad's 5-bin window per job, canonical pixel i -> pixel k
+    auto angle = [&](auto pat_tag, auto neg_tag, const float *w_base, float u, float ac) {
+        constexpr int P = decltype(pat_tag)::value;
+        constexpr bool NEG = decltype(neg_tag)::value;
+        constexpr int o1 = 0, o2 = P >= 2 ? 1 : 0, o3 = P == 0 ? 0 : P == 3 ? 2 : 1;
+        constexpr int oo[4] = {0, o1, o2, o3};
+        float w[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hat3(fmaf((float)i, ac, u) - (float)oo[i], w[i][0], w[i][1], w[i][2]);
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+            const float *wt = w_base + jj * (kQKC * kQW * BB);
+            float q[5][BB];
+#pragma unroll
+            for (int e = 0; e < 5; ++e) load_bins<BB>(wt + e * BB, q[e]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = NEG ? 3 - i : i;
+                tap3<BB>(acc[jj][k], w[i][0], w[i][1], w[i][2], q[oo[i]], q[oo[i] + 1], q[oo[i] + 2]);
+            }
+        }
+    };
+    for (int ch = 0; ch < nchunks; ++ch) {
+        const int bf = ch & 1;
+        if constexpr (BULK) {
+            mbar_wait(&full[bf], (unsigned)((ch >> 1) & 1));
+        } else {
+            if (ch + 1 < nchunks) stage(ch + 1, bf ^ 1);
+            if (ch + 1 < nchunks)
+                cp_async_wait<1>();
+            else
+                cp_async_wait<0>();
+            __syncthreads();
+        }
+        const int kc = min(kQKC, a.m - ch * kQKC);
+        const int tb = tbase(ch);
+#pragma unroll kQUnroll
+        for (int t = 0; t < kc; ++t) {
+            const float ct = s_cos[tb + t], st = s_sin[tb + t];
+            const int pt = s_pat[tb + t];
+            const float rowb = fmaf(-(float)ry, st, s_off[tb + t]);
+            const float t0 = fmaf((float)(4 * qc), ct, rowb);
+            const float tlow = (pt & 4) ? fmaf(3.f, ct, t0) : t0;  // the lowest of the 4
+            const float jf = floorf(fmaxf(tlow, 0.f));
+            const int j = min((int)jf, kQW - 5);
+            const float u = tlow - (float)j;
+            const float ac = fabsf(ct);
+            const float *wb = &win[bf][0][(t * kQW + j) * BB];
+            using I0 = std::integral_constant<int, 0>;
+            using I1 = std::integral_constant<int, 1>;
+            using I2 = std::integral_constant<int, 2>;
+            using I3 = std::integral_constant<int, 3>;
+            switch (pt) {
+                case 0: angle(I0{}, std::false_type{}, wb, u, ac); break;
+                case 1: angle(I1{}, std::false_type{}, wb, u, ac); break;
+                case 2: angle(I2{}, std::false_type{}, wb, u, ac); break;
+                case 3: angle(I3{}, std::false_type{}, wb, u, ac); break;
+                case 4: angle(I0{}, std::true_type{}, wb, u, ac); break;
+                case 5: angle(I1{}, std::true_type{}, wb, u, ac); break;
+                case 6: angle(I2{}, std::true_type{}, wb, u, ac); break;
+                default: angle(I3{}, std::true_type{}, wb, u, ac); break;
+            }
+        }
+        __syncthreads();  // buffer bf (and its table) is free for chunk ch + 2
+        if constexpr (BULK) {
+            if (ch + 2 < nchunks) produce(ch + 2, bf);
+        }
+    }
+
+    // ---- epilogue: scale and store; optional fused ei partials (job 0 = FBP)
+    const int r = tr0 + ry;
+    float eacc[BB];
+#pragma unroll
+    for (int b = 0; b < BB; ++b) eacc[b] = 0.f;
+    const int c = tc0 + 4 * qc;
+    if (r < a.row1) {
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                const AdjJob &jo = a.job[FUSED ? b : jj];
+                const int img = FUSED ? b0 : b0 + b;
+                const float sc = jo.scale;
+                const long o = (long)img * nn + (long)r * n + c;
+                const long ox = (long)img * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
+                float v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[k] = sc * acc[jj][k][b];
+                if (jo.base) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (c + k < n) v[k] += __ldg(jo.base + ox + k);
+                }
+                if (c + 3 < n && ((ox & 3) == 0)) {
+                    *reinterpret_cast<float4 *>(jo.x + ox) = make_float4(v[0], v[1], v[2], v[3]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (c + k < n) jo.x[ox + k] = v[k];
+                }
+                if (jj == 0 && (!FUSED || b == 0) && a.ei_x2) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (c + k < n) {
+                            const float d = __ldg(a.ei_x2 + o + k) - v[k];
+                            eacc[b] = fmaf(d, d, eacc[b]);
+                        }
+                }
+            }
+        }
+    }
+    if (!a.ei_x2) return;
+#pragma unroll
+    for (int b = 0; b < BB; ++b) {
+        float v = eacc[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_red[warp][b] = v;
+    }
+    __syncthreads();
+    const int ntiles = gridDim.x;
+    if (threadIdx.x < (FUSED ? 1 : BB)) {
+        float v = 0.f;
+        for (int w = 0; w < kThreads / 32; ++w) v += s_red[w][threadIdx.x];
+        a.ei_part[(long)(b0 + threadIdx.x) * ntiles + tile] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned total = gridDim.x * gridDim.y;
+        s_last = atomicAdd(a.ei_ctr, 1u) == total - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int b = warp; b < a.B; b += kThreads / 32) {
+        double sd = 0.0;
+        for (int i = lane; i < ntiles; i += 32) sd += (double)__ldcg(a.ei_part + (long)b * ntiles + i);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        if (lane == 0) a.ei_out[b] = (float)sd;
+    }
+    if (threadIdx.x == 0) *a.ei_ctr = 0u;
+}
+
+#ifndef SKEI_ADJ_QUAD
+#define SKEI_ADJ_QUAD 1  // bulk-staged backprojections use the quad kernel (A/B knob)
+#endif
+
+// the quad kernel's grid: 32 x 32 tiles (a.tiles_y is recomputed for its tile height)
+template <int BB, int NJ, bool BULK, bool FUSED>
+cudaError_t launch_quad(AdjArgs a, int ngroups, cudaStream_t s) {
+    a.tiles_y = (a.row1 - a.row0 + kQTileH - 1) / kQTileH;
+    dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)ngroups, 1);
+    k_radon_adj_quad<BB, NJ, BULK, FUSED><<<grid, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_fused(const AdjArgs &a, int B, cudaStream_t s) {
+    if (SKEI_ADJ_QUAD) return launch_quad<2, 1, true, true>(a, B, s);
     dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)B, 1);
     k_radon_adj<2, 1, true, true><<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
@@ -377,6 +669,15 @@ cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
     // bulk-copy staging needs 16-byte bins (BB = 4) and interleaved sources for every job
     constexpr bool kB4 = BB == 4;  // (the bulk variants are only instantiated for BB = 4)
     const bool bulk = kB4 && a.job[0].pi && (njobs == 1 || a.job[1].pi);
+    if (SKEI_ADJ_QUAD) {
+        if (bulk) {
+            if constexpr (kB4)
+                return njobs == 2 ? launch_quad<4, 2, true, false>(a, B / BB, s)
+                                  : launch_quad<4, 1, true, false>(a, B / BB, s);
+        }
+        return njobs == 2 ? launch_quad<BB, 2, false, false>(a, B / BB, s)
+                          : launch_quad<BB, 1, false, false>(a, B / BB, s);
+    }
     if (njobs == 2) {
         if (bulk)
             k_radon_adj<BB, 2, kB4><<<grid, kThreads, 0, s>>>(a);

@@ -79,6 +79,9 @@ constexpr int kKMax = 16;   // angles per CTA
 #define SKEI_FWD_AHEAD 1
 #endif
 constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ahead of use
+#ifndef SKEI_FWD_C3_ALWAYS
+#define SKEI_FWD_C3_ALWAYS 0  // load the fourth candidate unconditionally (A/B knob)
+#endif
 #ifndef SKEI_FWD_WIDE_SPLIT
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
@@ -582,7 +585,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     lds_px<BB>(pa, vv[0]);
                     lds_px<BB>(pa + kColF * sizeof(float), vv[1]);
                     lds_px<BB>(pa + 2 * kColF * sizeof(float), vv[2]);
+#if SKEI_FWD_C3_ALWAYS
+                    lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
+#else
                     if (fmaf(-ab, phi, off.z) < 1.f) lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
+#endif
                     if constexpr (kWide) {
                         if (fmaf(-ab, phi, off.w) < 1.f)
                             lds_px<BB>(pa + 4 * kColF * sizeof(float), vv[4]);
