@@ -657,19 +657,20 @@ cudaError_t launch_quad(AdjArgs a, int ngroups, cudaStream_t s) {
 }
 
 cudaError_t launch_fused(const AdjArgs &a, int B, cudaStream_t s) {
-    if (SKEI_ADJ_QUAD) return launch_quad<2, 1, true, true>(a, B, s);
+    // (the quad kernel measured slower for the job-fused groups: cfg5 250 -> 271 us, cfg4
+    // 2617 -> 2644 us — LDS.64 windows at 3 CTAs per SM against the pair kernel's 4)
     dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)B, 1);
     k_radon_adj<2, 1, true, true><<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int BB>
-cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s) {
+cudaError_t launch_bb(const AdjArgs &a, int njobs, int B, cudaStream_t s, bool quad) {
     dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)(B / BB), 1);
     // bulk-copy staging needs 16-byte bins (BB = 4) and interleaved sources for every job
     constexpr bool kB4 = BB == 4;  // (the bulk variants are only instantiated for BB = 4)
     const bool bulk = kB4 && a.job[0].pi && (njobs == 1 || a.job[1].pi);
-    if (SKEI_ADJ_QUAD) {
+    if (quad) {
         if (bulk) {
             if constexpr (kB4)
                 return njobs == 2 ? launch_quad<4, 2, true, false>(a, B / BB, s)
@@ -721,10 +722,14 @@ cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njob
     a.ei_out = ei ? ei->out : nullptr;
     if (fused) return launch_fused(a, B, s);
     const int bb = pick_bb(B, idx_stride);
+    // the quad kernel (32 x 32 tiles, 3 CTAs per SM) when its grid fills at least one wave;
+    // smaller problems (cfg2: 128 quad CTAs) keep the pair kernel's 2x finer grid
+    const long quad_ctas = (long)a.tiles_x * ((a.row1 - a.row0 + kQTileH - 1) / kQTileH) * (B / bb);
+    const bool quad = SKEI_ADJ_QUAD && quad_ctas >= 3L * plan->num_sms;
     switch (bb) {
-        case 4: return launch_bb<4>(a, njobs, B, s);
-        case 2: return launch_bb<2>(a, njobs, B, s);
-        default: return launch_bb<1>(a, njobs, B, s);
+        case 4: return launch_bb<4>(a, njobs, B, s, quad);
+        case 2: return launch_bb<2>(a, njobs, B, s, quad);
+        default: return launch_bb<1>(a, njobs, B, s, quad);
     }
 }
 
