@@ -82,6 +82,12 @@ constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ah
 #ifndef SKEI_FWD_C3_ALWAYS
 #define SKEI_FWD_C3_ALWAYS 0  // load the fourth candidate unconditionally (A/B knob)
 #endif
+#ifndef SKEI_FWD_STATS_EVERY
+#define SKEI_FWD_STATS_EVERY 37  // -DSKEI_FWD_STATS: print the counters of every n-th CTA
+#endif
+#ifndef SKEI_FWD_STRIDED
+#define SKEI_FWD_STRIDED 1  // a unit takes every ng-th angle of its class (A/B knob)
+#endif
 #ifndef SKEI_FWD_WIDE_SPLIT
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
@@ -380,7 +386,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         const int b0 = FUSED ? d.q : d.q * BB;  // the group's first image (fused: its image)
         const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
 
-        // ---- 2. the unit's K angles (grp-th group of class cls, sketch-slot order) + geometry
+        // ---- 2. the unit's angles + geometry: the class's angles (in sketch order) are dealt to
+        // its ngc = ceil(n_class / K) units round-robin, unit grp taking ranks grp, grp + ngc, ...
+        // (strided: every unit mixes angles from the whole class range, so units cost about
+        // the same — a unit of consecutive angles near 0 degrees projects onto ~1.4x the bins
+        // of one near 45 — and sizes differ by at most one angle)
+        const int ncls = d.cls == 0 ? s_nrow[d.q] : a.m - s_nrow[d.q];
+        const int ngc = (ncls + K - 1) / K;
+        (void)ngc;
         if (warp == 0) {
             int seen = 0;
             for (int base = 0; base < a.m; base += 32) {
@@ -393,12 +406,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
                 const int pre = seen + __popc(bal & ((1u << lane) - 1u));
+#if SKEI_FWD_STRIDED
+                if (in && pre % ngc == d.grp) sSlot[pre / ngc] = k;
+#else
                 if (in && pre >= d.grp * K && pre < d.grp * K + K) sSlot[pre - d.grp * K] = k;
+#endif
                 seen += __popc(bal);
             }
-            if (lane == 0) sCount = max(0, min(K, seen - d.grp * K));
+#if SKEI_FWD_STRIDED
+            const int cnt = max(0, (seen - d.grp + ngc - 1) / ngc);
+#else
+            const int cnt = max(0, min(K, seen - d.grp * K));
+#endif
+            if (lane == 0) sCount = cnt;
             __syncwarp();
-            if (lane < min(K, max(0, seen - d.grp * K))) {
+            if (lane < cnt) {
                 const double2 cs = a.g.trig[idx[sSlot[lane]]];
                 const double c = cs.x, sn = cs.y, h = a.g.h, hd = a.g.hd;
                 double P0, Pj, Pl, ab;
@@ -826,6 +848,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         const FwdJob job = d.job ? a.job[1] : a.job[0];
         const int b0 = FUSED ? d.q : d.q * BB;
         const int32_t *idx = a.idx + (a.idx_stride ? (long)b0 * a.idx_stride : 0);
+        const int ncls = d.cls == 0 ? s_nrow[d.q] : a.m - s_nrow[d.q];
+        const int ngc = (ncls + K - 1) / K;
+        (void)ngc;
         __syncthreads();  // sSlot free
         if (warp == 0) {  // the unit's angle slots, as in step 2
             int seen = 0;
@@ -839,10 +864,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
                 const int pre = seen + __popc(bal & ((1u << lane) - 1u));
+#if SKEI_FWD_STRIDED
+                if (in && pre % ngc == d.grp) sSlot[pre / ngc] = k;
+#else
                 if (in && pre >= d.grp * K && pre < d.grp * K + K) sSlot[pre - d.grp * K] = k;
+#endif
                 seen += __popc(bal);
             }
+#if SKEI_FWD_STRIDED
+            if (lane == 0) sCount = max(0, (seen - d.grp + ngc - 1) / ngc);
+#else
             if (lane == 0) sCount = max(0, min(K, seen - d.grp * K));
+#endif
         }
         __syncthreads();
         const int total = sCount * n_det, npc = s_dnpc[di];
@@ -922,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #endif
 
 #ifdef SKEI_FWD_STATS
-    if (lane == 0 && (blockIdx.x % 37) == 0)
+    if (lane == 0 && (blockIdx.x % SKEI_FWD_STATS_EVERY) == 0)
         printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld active %lld "
                "lanes %lld esync %lld fin %lld\n", blockIdx.x, warp, u_last - u_first + 1, G, st_wait,
                st_pro, st_epi, clock64() - st_t0, st_active, st_lanes, 0LL, st_fin);
