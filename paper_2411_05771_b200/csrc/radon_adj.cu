@@ -383,13 +383,20 @@ constexpr int kQKC = 12;     // angles per staged chunk
 #ifndef SKEI_ADJQ_MINB
 #define SKEI_ADJQ_MINB 3     // CTAs per SM the quad kernel is compiled for
 #endif
+#ifndef SKEI_ADJQ_MINB_FUSED
+#define SKEI_ADJQ_MINB_FUSED 4  // ... for job-fused groups (8 accumulators per thread)
+#endif
+#ifndef SKEI_ADJQ_FUSED
+#define SKEI_ADJQ_FUSED 1    // job-fused groups use the quad kernel (A/B knob)
+#endif
 #ifndef SKEI_ADJQ_UNROLL
 #define SKEI_ADJQ_UNROLL 1   // angles unrolled in the quad kernel's loop
 #endif
 constexpr int kQUnroll = SKEI_ADJQ_UNROLL;
 
 template <int BB, int NJ, bool BULK, bool FUSED>
-__global__ void __launch_bounds__(kThreads, SKEI_ADJQ_MINB) k_radon_adj_quad(AdjArgs a) {
+__global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_ADJQ_MINB)
+    k_radon_adj_quad(AdjArgs a) {
     __shared__ __align__(128) float win[2][NJ][kQKC * kQW * BB];
     __shared__ float s_off[kTab], s_cos[kTab], s_sin[kTab];
     __shared__ int s_w0[kTab], s_pat[kTab];
@@ -657,8 +664,10 @@ cudaError_t launch_quad(AdjArgs a, int ngroups, cudaStream_t s) {
 }
 
 cudaError_t launch_fused(const AdjArgs &a, int B, cudaStream_t s) {
-    // (the quad kernel measured slower for the job-fused groups: cfg5 250 -> 271 us, cfg4
-    // 2617 -> 2644 us — LDS.64 windows at 3 CTAs per SM against the pair kernel's 4)
+    if (SKEI_ADJQ_FUSED) return launch_quad<2, 1, true, true>(a, B, s);
+    // job-fused groups: the quad kernel compiled for 4 CTAs per SM (64 registers; 8
+    // accumulators per thread): cfg4 2618 -> 2369 us, cfg5 250 -> 236 us against the pair
+    // kernel (at 3 CTAs per SM it was slower: 2644 / 268 us)
     dim3 grid((unsigned)(a.tiles_x * a.tiles_y), (unsigned)B, 1);
     k_radon_adj<2, 1, true, true><<<grid, kThreads, 0, s>>>(a);
     return cudaGetLastError();
