@@ -88,6 +88,9 @@ constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ah
 #ifndef SKEI_FWD_STRIDED
 #define SKEI_FWD_STRIDED 1  // a unit takes every ng-th angle of its class (A/B knob)
 #endif
+#ifndef SKEI_FWD_WHOLE
+#define SKEI_FWD_WHOLE 1  // whole units per CTA when there are 0.9 - 1 units per CTA (A/B knob)
+#endif
 #ifndef SKEI_FWD_WIDE_SPLIT
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
@@ -306,7 +309,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     // piece to finish (per-unit counter) adds the pieces in CTA order and finishes the unit.
     const int nbc = a.nblk;
     const long W = (long)total_units * nbc;
-    auto wstart = [&](int c) -> long { return (long)c * W / ncl; };
+    // nearly one unit per CTA (0.9 ncl <= U <= ncl, e.g. cfg3's 144 units on 148 SMs): whole
+    // units, one per CTA — no split units, so no piece stores, fix-ups or second prologue /
+    // epilogue, for at most 1/0.9 of the per-CTA blocks
+    const bool whole = SKEI_FWD_WHOLE && total_units <= ncl && 10L * total_units >= 9L * ncl;
+    auto wstart = [&](int c) -> long {
+        return whole ? (long)min(c, total_units) * nbc : (long)c * W / ncl;
+    };
     const long w0 = wstart(cid), w1 = wstart(cid + 1);
     const int u_first = (int)(w0 / nbc), u_last = w1 > w0 ? (int)((w1 - 1) / nbc) : u_first - 1;
     auto cta_of = [&](long w) -> int {  // the CTA whose range holds block w
