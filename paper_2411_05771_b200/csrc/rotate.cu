@@ -183,6 +183,28 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     }
     const long grp = (long)blockIdx.y * a.nblk * n * 32;  // floats per image group per class
     const int lim = a.nblk * R;                            // packed lines (incl. zero padding)
+    if (R == 8 && r0 + kT <= lim && c0 + kT <= n && r0 + kT <= n && c0 + kT <= lim) {
+        // interior tile (BB = 4): for a fixed block of 8 lines the tile's 32 pixels x 8 lines
+        // are 4 KB of contiguous packed output, so thread t stores the 16-byte slot t of each
+        // of the 4 blocks (pixel t / 8, line t % 8): one LDS.128 + one STG.128 per slot, the
+        // addresses one add apart (no per-slot index arithmetic or bounds checks)
+        const int px = threadIdx.x >> 3, ln = threadIdx.x & 7;
+        if (job.xr) {  // row blocks r0 / 8 + rb: pixel = column c0 + px, line = row rb * 8 + ln
+            V *dst = reinterpret_cast<V *>(job.xr + grp + ((long)(r0 >> 3) * n + c0) * 32) + threadIdx.x;
+            const float *src = tile + ln * kRow + px * BB;
+#pragma unroll
+            for (int rb = 0; rb < kT / 8; ++rb)
+                dst[(long)rb * n * 8] = *reinterpret_cast<const V *>(src + rb * 8 * kRow);
+        }
+        if (job.xc) {  // column blocks c0 / 8 + cb: pixel = row r0 + px, line = column cb * 8 + ln
+            V *dst = reinterpret_cast<V *>(job.xc + grp + ((long)(c0 >> 3) * n + r0) * 32) + threadIdx.x;
+            const float *src = tile + px * kRow + ln * BB;
+#pragma unroll
+            for (int cb = 0; cb < kT / 8; ++cb)
+                dst[(long)cb * n * 8] = *reinterpret_cast<const V *>(src + cb * 8 * BB);
+        }
+        return;
+    }
     // each item is one pixel-line slot of BB floats (16 / 8 / 4 bytes); consecutive threads
     // take consecutive slots of a packed 128-byte pixel column
     if (job.xr) {  // row-packed: block r / R, pixel c, line r % R
