@@ -565,6 +565,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const float4 ang = sAng[k];   // |beta|, 1/|beta|, Pl, min(Pj, 0)
                 const float4 off = sAng2[k];  // hat offsets 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2
                 const float ab = ang.x, plf = ang.z;
+                // 1 - (d3 - 1) = |b| phi + (3 - 4|b|) and likewise for d4: the upper bin's
+                // weights of c3 / c4 in one FFMA (their loads are predicated on the same value)
+                const float k3 = 1.f - off.z, k4 = 1.f - off.w;
                 // a candidate window of 5 pixels can be needed only if 4|beta| - 1 < 2
                 const bool wide = off.z < 1.f;
                 // + (2 lane - 31) Pj (|.| < 44, fp32): the lane's lower bin within the chunk
@@ -619,10 +622,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
 #if SKEI_FWD_C3_ALWAYS
                     lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
 #else
-                    if (fmaf(-ab, phi, off.z) < 1.f) lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
+                    if (fmaf(ab, phi, k3) > 0.f) lds_px<BB>(pa + 3 * kColF * sizeof(float), vv[3]);
 #endif
                     if constexpr (kWide) {
-                        if (fmaf(-ab, phi, off.w) < 1.f)
+                        if (fmaf(ab, phi, k4) > 0.f)
                             lds_px<BB>(pa + 4 * kColF * sizeof(float), vv[4]);
                     }
                 };
@@ -630,10 +633,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     const float w0 = fmaf(-ab, phi, ab);
                     const float d1 = fmaf(-ab, phi, off.x);
                     const float e2 = fmaf(-ab, phi, off.y);
-                    const float e3 = fmaf(-ab, phi, off.z);
                     const float w1 = 1.f - fabsf(d1), u1 = fmaxf(d1, 0.f);
                     const float w2 = fmaxf(-e2, 0.f), u2 = 1.f - fabsf(e2);
-                    const float u3 = fmaxf(1.f - e3, 0.f);
+                    const float u3 = fmaxf(fmaf(ab, phi, k3), 0.f);
                     fma_px<BB>(lo, w0, vv[0]);
                     fma_px<BB>(lo, w1, vv[1]);
                     fma_px<BB>(hi, u1, vv[1]);
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     fma_px<BB>(hi, u2, vv[2]);
                     fma_px<BB>(hi, u3, vv[3]);
                     if constexpr (kWide) {
-                        const float u4 = fmaxf(1.f - fmaf(-ab, phi, off.w), 0.f);
+                        const float u4 = fmaxf(fmaf(ab, phi, k4), 0.f);
                         fma_px<BB>(hi, u4, vv[4]);
                     }
                 };
