@@ -248,6 +248,35 @@ def test_pass_parity_full_size_class_boundary_angles(g):
             assert abs(float(out[k][b]) - ref[k]) <= TOL * abs(ref[k]), (k, b)
 
 
+def test_quad_backprojector_ragged_tiles_all_patterns():
+    """The quad backprojector (32 x 32 tiles, four pixels per thread; chosen when its grid
+    fills a wave) at N = 500 — ragged last tiles in both directions — with a sketch of every
+    other angle of 60 (0, 6, ..., 174 degrees), so every per-angle window pattern (|cos| in
+    [0, 1/3], (1/3, 1/2], (1/2, 2/3], (2/3, 1]) occurs with both signs of cos: the standalone
+    adjoint and FBP (plain staging) for all 8 images, and the pass (bulk staging, fused EI)
+    for two images, against the oracle."""
+    N, n_det, n_full, B = 500, 708, 60, 8
+    plan = sk.Plan.get(N, n_det, n_full, 0)
+    idx = np.arange(0, n_full, 2, dtype=np.int32)
+    m = len(idx)
+    y = synth.rand_sinograms(B, m, n_det, 11)
+    x = sk.radon_adj(plan, dev(y), idx_t(idx), 2.0)
+    xf = sk.fbp(plan, dev(y), idx_t(idx))
+    for b in range(B):
+        close(x[b], oracle.adj(y[b], idx, n_full, N, 2.0), f"quad adj b={b}")
+        close(xf[b], oracle.fbp(y[b], idx, n_full, N), f"quad fbp b={b}")
+    x1 = synth.rand_images(B, N, 12)
+    yf = synth.rand_sinograms(B, n_full, n_det, 13)
+    out = sk.sketched_pass(plan, dev(x1), dev(yf), idx_t([73]), idx_t(idx[None]))
+    torch.cuda.synchronize()
+    for b in (0, B - 1):
+        ref = oracle.sketched_pass(x1[b], yf[b], 73, idx, n_full)
+        for k in ("x2", "p1", "p2", "q", "xfbp", "r", "grad"):
+            close(out[k][b], ref[k], f"quad pass {k} b={b}")
+        for k in ("mc", "ei"):
+            assert abs(float(out[k][b]) - ref[k]) <= TOL * abs(ref[k]), (k, b)
+
+
 @pytest.mark.parametrize("N,n_det,n_full,P,B,m", [
     (1536, 2173, 32, 8192, 1, 4),   # the largest image the ABI accepts (n <= 1536), P = 8192
     (256, 3072, 16, 8192, 4, 4),    # the widest detector (n_det <= 3072): one angle per unit
