@@ -25,6 +25,14 @@ namespace {
 
 constexpr int kT = 32;          // tile side (pixels)
 constexpr int kThreads = 256;   // 32 columns x 8 row groups; a thread owns 4 rows
+// staged rotation (shared g, groups of 4): the tile's source footprint, <= 31 (|cos| + |sin|)
+// + 2 taps + 2 guard pixels <= 47 per side, staged as [row][col][image] with an odd pixel
+// pitch (16-byte slots: a quarter-warp's bilinear taps spread over the bank groups)
+constexpr int kSrc = 48, kSrcPitch = 49;
+constexpr int kStageF = kSrc * kSrcPitch * 4;
+#ifndef SKEI_ROT_STAGED
+#define SKEI_ROT_STAGED 1  // shared-g rotations of groups of 4 via the staged footprint (A/B knob)
+#endif
 
 struct RotOrigin {
     int bc, br;      // integer part of the tile origin's source column / row
@@ -45,7 +53,10 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     constexpr int R = 32 / BB;
     using V = typename VecT<BB>::T;
     constexpr int kRow = kT * BB + 4;  // padded tile row (floats)
-    __shared__ __align__(16) float tile[kT * kRow];
+    // the output tile (packing) — overlaid, in the staged rotation, on the source footprint
+    constexpr int kSmemF = kStageF > kT * kRow ? kStageF : kT * kRow;
+    __shared__ __align__(16) float smraw[kSmemF];
+    float *const tile = smraw;
     __shared__ RotOrigin sRot[BB];
     const RotPackJob job = blockIdx.z ? a.job[1] : a.job[0];
     const int n = a.n;
@@ -77,7 +88,71 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
     // of one tile column: consecutive source positions then step by |cos g| < |sin g| rows
     // (instead of |sin g| per column), so a warp's bilinear taps stay within a few cache
     // lines; the plain output is then written from the staged tile (coalesced)
-    const bool swp = job.g != nullptr && fabsf(sRot[0].sg) > fabsf(sRot[0].cg);
+    const bool staged = SKEI_ROT_STAGED && BB == 4 && !XM && job.g != nullptr && job.g_stride == 0;
+    const bool swp = !staged && job.g != nullptr && fabsf(sRot[0].sg) > fabsf(sRot[0].cg);
+    if (staged) {
+        // ---- staged rotation: the source footprint of the output tile, zero outside the
+        // image, is copied once (coalesced rows, 4 images interleaved per pixel); every
+        // bilinear tap is then one LDS.128 for the 4 images, with no bounds predicates.
+        // Same weights, same FMA order as the direct path (outside taps add w * 0).
+        const RotOrigin o = sRot[0];
+        const float e = 31.f;
+        const float cmn = o.fc + fminf(0.f, e * o.cg) + fminf(0.f, -e * o.sg);
+        const float rmn = o.fr + fminf(0.f, e * o.sg) + fminf(0.f, e * o.cg);
+        const int clo = o.bc + (int)floorf(cmn) - 1, rlo = o.br + (int)floorf(rmn) - 1;
+        for (int it = threadIdx.x; it < kSrc * kSrc; it += kThreads) {
+            const int i = it / kSrc, j = it - i * kSrc;
+            const int r = rlo + i, c = clo + j;
+            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r >= 0 && r < n && c >= 0 && c < n) {
+                const float *xp = job.x + (long)b0 * nn + (long)r * n + c;
+                t.x = __ldg(xp);
+                if (b0 + 1 < a.B) t.y = __ldg(xp + nn);
+                if (b0 + 2 < a.B) t.z = __ldg(xp + 2 * nn);
+                if (b0 + 3 < a.B) t.w = __ldg(xp + 3 * nn);
+            }
+            *reinterpret_cast<float4 *>(smraw + (i * kSrcPitch + j) * 4) = t;
+        }
+        __syncthreads();
+        float4 res[kT / 8];
+#pragma unroll
+        for (int i = 0; i < kT / 8; ++i) {
+            const int rr = tr + 8 * i, cc = tc;
+            const float dr = (float)rr, dc = (float)cc;
+            const float cl = o.fc + fmaf(dc, o.cg, -dr * o.sg);
+            const float rl = o.fr + fmaf(dc, o.sg, dr * o.cg);
+            const float flc = floorf(cl), flr = floorf(rl);
+            const float fb = cl - flc, fa = rl - flr;
+            const int ci = o.bc + (int)flc - clo, ri = o.br + (int)flr - rlo;
+            SKEI_DCHECK(ci >= 0 && ci + 1 < kSrc && ri >= 0 && ri + 1 < kSrc, "rotation footprint");
+            const float *sp = smraw + (ri * kSrcPitch + ci) * 4;
+            const float4 x00 = *reinterpret_cast<const float4 *>(sp);
+            const float4 x01 = *reinterpret_cast<const float4 *>(sp + 4);
+            const float4 x10 = *reinterpret_cast<const float4 *>(sp + kSrcPitch * 4);
+            const float4 x11 = *reinterpret_cast<const float4 *>(sp + kSrcPitch * 4 + 4);
+            const float w00 = (1.f - fa) * (1.f - fb), w01 = (1.f - fa) * fb;
+            const float w10 = fa * (1.f - fb), w11 = fa * fb;
+            float4 v;
+            v.x = fmaf(w11, x11.x, fmaf(w10, x10.x, fmaf(w01, x01.x, fmaf(w00, x00.x, 0.f))));
+            v.y = fmaf(w11, x11.y, fmaf(w10, x10.y, fmaf(w01, x01.y, fmaf(w00, x00.y, 0.f))));
+            v.z = fmaf(w11, x11.z, fmaf(w10, x10.z, fmaf(w01, x01.z, fmaf(w00, x00.z, 0.f))));
+            v.w = fmaf(w11, x11.w, fmaf(w10, x10.w, fmaf(w01, x01.w, fmaf(w00, x00.w, 0.f))));
+            const int r = r0 + rr, c = c0 + cc;
+            if (r >= n || c >= n) v = make_float4(0.f, 0.f, 0.f, 0.f);
+            res[i] = v;
+            if (job.out && r < n && c < n) {
+                const long o2 = (long)b0 * nn + (long)r * n + c;
+                job.out[o2] = v.x;
+                if (b0 + 1 < a.B) job.out[o2 + nn] = v.y;
+                if (b0 + 2 < a.B) job.out[o2 + 2 * nn] = v.z;
+                if (b0 + 3 < a.B) job.out[o2 + 3 * nn] = v.w;
+            }
+        }
+        __syncthreads();  // footprint reads done: the tile overlays it
+#pragma unroll
+        for (int i = 0; i < kT / 8; ++i)
+            *reinterpret_cast<float4 *>(tile + (tr + 8 * i) * kRow + tc * BB) = res[i];
+    } else {
 #pragma unroll
     for (int i = 0; i < kT / 8; ++i) {
         const int rr = swp ? tc : tr + 8 * i, r = r0 + rr;
@@ -140,6 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
 #pragma unroll
         for (int b = 0; b < BB; ++b) tp[b] = v[b];
         *reinterpret_cast<V *>(tile + rr * kRow + cc * BB) = t;
+    }
     }
     const bool late_out = swp && job.out;
     if (!job.xr && !job.xc && !late_out) return;
