@@ -113,6 +113,7 @@ def rank_env():
 STAGES = ["rotate_pack", "radon_fwd_x2", "ramp", "radon_adj_x2"]
 LAUNCHES_PER_STEP = 5  # draw, rotate+pack, forward (2 jobs + MC), ramp, adjoint (2 jobs + EI)
 E2E_SLOTS = 3  # e2e pipeline depth (slots of device buffers and streams)
+E2E_REPS = 3  # e2e: repetitions of the K timed steps (the median is reported)
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -824,21 +825,32 @@ def main():
         torch.cuda.synchronize()
         for sl in slots:
             sl["done"] = None
-        t0 = time.perf_counter()
-        for i in range(args.steps):
-            e2e_step(1000 + i)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        # E2E_REPS back-to-back repetitions of the K steps, each timed on its own (max over
+        # ranks); the line reports the median repetition — the host wall clock of one
+        # repetition is exposed to host scheduling hiccups of the box
+        reps = []
+        for rep in range(E2E_REPS):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                e2e_step(1000 + rep * args.steps + i)
+            torch.cuda.synchronize()
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t.item())
+            reps.append(el)
+        el = float(np.median(reps))
         # a shared sketch copies only y's m sketched rows (skei_pass_host), else all of y
         y_h2d = B * m * cfg.n_det * 4 if shared else hy.numel() * 4
         h2d = hx1.numel() * 4 + y_h2d + ng * 4 + ng * m * 4
         d2h = 2 * B * 4 + (B * N * N * 4 if args.e2e_grad else 0)
         e2e = {"value": passes_per_step * args.steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "reps": [passes_per_step * args.steps / r for r in reps],
                "returns": "mc, ei and the MC gradient" if args.e2e_grad else
                           "mc, ei (the gradient and x_fbp stay on the device; --e2e-grad reads "
                           "the gradient back too)",
@@ -847,7 +859,8 @@ def main():
                          "library; all of y for per-image sketches), g, idx "
                          "from pinned memory, the pass, D2H of its results, in-stream L2 flush "
                          "(256 MB write) behind it; slots with their own streams rotate, so one "
-                         "step's H2D overlaps the previous steps' passes (3 slots)"}
+                         "step's H2D overlaps the previous steps' passes (3 slots); the median "
+                         f"of {E2E_REPS} repetitions of the K steps"}
 
     if rank != 0:
         if world > 1:
