@@ -235,8 +235,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int done[3];  // warps that finished each buffer (monotonic)
     __shared__ double sP0[kKMax], sPj[kKMax], sPl[kKMax];
     __shared__ float sAbsB[kKMax];
-    __shared__ float4 sAng[kKMax];   // |beta|, 1/|beta|, Pl, min(Pj, 0) (fp32)
-    __shared__ float4 sAng2[kKMax];  // 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2 (hat offsets)
+    // per unit angle k, one 48-byte record (one base address per task in the block loop):
+    // [0] |beta|, 1/|beta|, Pl, min(Pj, 0); [1] hat offsets 2|b| - 1, 3|b| - 2, 4|b| - 2,
+    // 5|b| - 2; [2].x Pj (all fp32)
+    __shared__ float4 sAngT[kKMax][3];
     __shared__ int sSlot[kKMax];
     __shared__ int sCount;
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
@@ -246,7 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     __shared__ int s_cost[kWarps * kMaxT];   // per task: blocks its chunk touches
     __shared__ int s_defer[2], s_dnpc[2];  // split units this CTA finishes after its stream
     __shared__ int s_dpiece[2][kMaxPieces];  // ... their piece slots in CTA order
-    __shared__ float sPjf[kKMax];            // Pj (fp32)
 
     const int cid = blockIdx.x, ncl = gridDim.x;
     const int n = a.g.n, n_det = a.g.n_det, n_full = a.g.n_full;
@@ -446,12 +447,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 }
                 sP0[lane] = P0;
                 sPj[lane] = Pj;
-                sPjf[lane] = (float)Pj;
                 sPl[lane] = Pl;
                 sAbsB[lane] = (float)ab;
-                sAng[lane] = make_float4((float)ab, (float)(1.0 / ab), (float)Pl,
+                sAngT[lane][2] = make_float4((float)Pj, 0.f, 0.f, 0.f);
+                sAngT[lane][0] = make_float4((float)ab, (float)(1.0 / ab), (float)Pl,
                                          (float)fmin(Pj, 0.0));
-                sAng2[lane] = make_float4((float)(2.0 * ab - 1.0), (float)(3.0 * ab - 2.0),
+                sAngT[lane][1] = make_float4((float)(2.0 * ab - 1.0), (float)(3.0 * ab - 2.0),
                                           (float)(4.0 * ab - 2.0), (float)(5.0 * ab - 2.0));
             }
         }
@@ -562,8 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                     frac -= 1.f;
                     base += 1;
                 }
-                const float4 ang = sAng[k];   // |beta|, 1/|beta|, Pl, min(Pj, 0)
-                const float4 off = sAng2[k];  // hat offsets 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2
+                const float4 ang = sAngT[k][0];  // |beta|, 1/|beta|, Pl, min(Pj, 0)
+                const float4 off = sAngT[k][1];  // hat offsets 2|b| - 1, 3|b| - 2, 4|b| - 2, 5|b| - 2
                 const float ab = ang.x, plf = ang.z;
                 // 1 - (d3 - 1) = |b| phi + (3 - 4|b|) and likewise for d4: the upper bin's
                 // weights of c3 / c4 in one FFMA (their loads are predicated on the same value)
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 // a candidate window of 5 pixels can be needed only if 4|beta| - 1 < 2
                 const bool wide = off.z < 1.f;
                 // + (2 lane - 31) Pj (|.| < 44, fp32): the lane's lower bin within the chunk
-                const float fs = fmaf(lane2f, sPjf[k], frac - ang.y);
+                const float fs = fmaf(lane2f, sAngT[k][2].x, frac - ang.y);
                 // candidate_0 + kCand = base + 6 + floor(e); floor(e) is taken as an exact
                 // fp32 integer and moved to the integer unit by the 1.5 * 2^23 bias (|e| < 2^22)
                 const int base6 = base + 1 + kCand - 0x4B400000;
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         // the lane's pair (j0, j0 + 1) of task t: acc holds (lower, upper); the lower bin is
         // j0 unless Pj < 0
         auto pair_sums = [&](int t, float (&s0)[BB], float (&s1)[BB]) {
-            const bool neg = sAng[s_task[warp + kWarps * t].x].w < 0.f;
+            const bool neg = sAngT[s_task[warp + kWarps * t].x][0].w < 0.f;
 #pragma unroll
             for (int b = 0; b < BB; ++b) {
                 s0[b] = neg ? acc[t][BB + b] : acc[t][b];
