@@ -24,6 +24,9 @@
 //   * Optional fused epilogue (skei_pass with the identity network): ei partial sums
 //     sum (x2 - x_fbp)^2 per tile and image, reduced in fixed order by the last CTA.
 // Work per (pixel, angle, image) = 2 taps; per pixel pair and angle 3 LDS.BB per job.
+//   * k_radon_adj_quad (below): the same with FOUR adjacent pixels per thread (one 5-bin
+//     window per angle and job serves them; 32 x 32 tiles) — used wherever its grid fills a
+//     wave, and for the job-fused groups; the pair kernel serves the small grids.
 #include <type_traits>
 
 #include "internal.h"

@@ -20,6 +20,7 @@
 //     CTA per SM) and stream-K scheduled: the U x nblk (unit, line block) work is cut into
 //     equal contiguous ranges, one per CTA, so every SM streams the same number of blocks;
 //     a unit cut by a range boundary is finished by the last of its pieces (see step 4).
+//     With 0.9-1 units per CTA (cfg3: 144 units on 148 SMs) every CTA takes one whole unit.
 //     The block stream continues across units, so the next unit's first blocks are in
 //     flight while the current unit's epilogue runs.
 //   * Bank-conflict-free gathers: lane L visits the lines of a block in the order
@@ -28,20 +29,27 @@
 //     banks, whatever pixel each lane's bin needs (a lane-per-bin layout gives 2-way
 //     conflicts at every angle with |beta| < 1 because 8 bins span more than 8 pixels), and
 //     consecutive lines differ in one bit, so the position moves by one add per line.
-//   * 512 threads (128 registers each), one CTA per SM.  Task = (angle, 32 consecutive
-//     bins), lane = bin; a thread owns up to kMaxT = 8 tasks and keeps BB accumulators per
-//     task in registers: K = 16 kMaxT / chunks angles per unit.  Per unit the block table
-//     counts, for every chunk, the blocks it touches; chunks touching none are dropped
-//     (their bins written as 0) and the rest dealt to the 16 warps by that cost in snake
-//     order.  A warp's next task descriptor is loaded one task ahead.
+//   * 512 threads (<= 128 registers each), one CTA per SM.  Task = (angle, 64 consecutive
+//     bins); lane L owns the bin pair (c0 + 2L, c0 + 2L + 1), whose line positions differ by
+//     1/|beta|, so per line the pair needs the 3-5 consecutive candidate pixels c0..c4: c0
+//     feeds the lower bin, c1 and c2 both, c3 (and c4) the upper one.  A thread owns up to
+//     kMaxT tasks (4 for groups of 4 images) and keeps 2 x BB accumulators per task in
+//     registers: K = 16 kMaxT / chunks angles per unit.  A class's angles are dealt to its
+//     units round-robin (every unit mixes angles from the whole class range, so units cost
+//     about the same).  Per unit the block table counts, for every chunk, the blocks it
+//     touches; chunks touching none are dropped (their bins written as 0) and the rest dealt
+//     to the 16 warps by that cost in snake order.  A warp's next task descriptor is loaded
+//     one task ahead.  The line loop is compiled with and without the fifth candidate and
+//     picked per task (warp-uniform: |beta| of the task's angle).
 //   * Decoupled pipeline: no per-block barrier.  The last warp to finish a staged block
 //     (shared-memory counter) refills its buffer with the block nbuf ahead, so warps drift
 //     up to nbuf - 1 blocks apart and per-block load imbalance averages out.
-//   * Per (bin, line): a* from an fp64 per-block base plus an fp32 offset (split precision,
-//     DESIGN.md §5), 3 hat weights, 3 LDS.BB (the third skipped when its weight is 0) issued
-//     kAhead = 1 line ahead of use, 3*BB FMAs as packed fp32x2 FFMA2.  The R lines of a block are
-//     summed into a partial before it is added to the running total (two-level summation).
-//     A chunk skips a block none of its 32 bins sees.
+//   * Per (bin pair, line): the lower bin's line position from an fp64 per-block base plus
+//     an fp32 offset (split precision), floor / fraction, one unsigned-min clamp
+//     into the zero pad columns, 7 hat weights, 3-5 LDS.BB (c3 / c4 only where their weight
+//     is > 0) issued kAhead = 1 line ahead of use, 6-7 x BB/2 packed fp32x2 FFMA2.  The R lines
+//     of a block are summed into a partial before it is added to the running total
+//     (two-level summation).  A chunk skips a block none of its bins sees.
 //   * Unit end: a whole unit's sums are complete in registers -> p; for the MC job also
 //     r = p - y_S and per-unit partial sums of r^2, summed in a fixed order by the last CTA
 //     to finish (completion counter).  A split unit's pieces go to L2 slots and the last

@@ -15,7 +15,10 @@
 // TMA bulk copy per block.  Pixels outside the image (the last block's
 // padding lines) are written as zeros.  The identity job (g = 0, no taps) packs x1.  With a
 // shared g the BB images share one set of taps per pixel; for |sin g| > |cos g| a warp's
-// lanes take 32 rows of one column (taps stay within a few cache lines).  Behind the pass's
+// lanes take 32 rows of one column (taps stay within a few cache lines).  A shared g on a
+// group of 4 instead stages the tile's source footprint (<= 47 x 47 pixels, zero outside the
+// image) in shared memory, 4 images interleaved per pixel, so each tap is one LDS.128 with
+// no bounds predicates (same weights and FMA order).  Behind the pass's
 // own draw kernel (skei_pass_draw) the launch is programmatically serialised: only the
 // rotation job waits (griddepcontrol.wait) for g.
 #include "internal.h"
