@@ -9,6 +9,10 @@
 
 #include "internal.h"
 
+#ifndef SKEI_PACK_ONE
+#define SKEI_PACK_ONE 1  // groups of 4: one (row-) packed copy per image, columns via a tensor map
+#endif
+
 using namespace skei;
 
 namespace {
@@ -574,11 +578,14 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     // image's x1 and x2 share its sketch, so they are the two slots of one group of the
     // forward (one set of per-(bin, line) geometry for both), packed together: the fused
     // row-packed copy spans pack[0..1], the column-packed one pack[2..3]
+    // Groups of 4 pack only the row-lines copy of x1 and x2: the forward stages the column
+    // class from it through a transposing tensor map (half the packing traffic)
     const bool fuse = fwd_bb(B, idx_stride) == 1;
+    const bool one = SKEI_PACK_ONE && fwd_bb(B, idx_stride) == 4;
     RotPackJob rj[2] = {
-        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[fuse ? 2 : 1]), ctr},
-        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[fuse ? 0 : 2]), ws_f(ws, wl.pack[fuse ? 2 : 3]),
-         nullptr}};
+        {x1, nullptr, nullptr, 0, ws_f(ws, wl.pack[0]), one ? nullptr : ws_f(ws, wl.pack[fuse ? 2 : 1]), ctr},
+        {x1, o->x2, g_deg, g_stride, ws_f(ws, wl.pack[fuse ? 0 : 2]),
+         one ? nullptr : ws_f(ws, wl.pack[fuse ? 2 : 3]), nullptr}};
     SKEI_CUDA(launch_rotate_pack(plan, rj, 2, B, fwd_bb(B, idx_stride), s, draw != nullptr, fuse));
     SKEI_CUDA(mark(1));
     // a3 + a7 (MC part): p1 = A_S x1 with r = p1 - y_S and mc = ||r||^2 fused into its
@@ -589,8 +596,9 @@ skei_status run_pass(const skei_plan *plan, int32_t B, const float *x1, const fl
     const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
     float *qi = il || fuse ? ws_f(ws, wl.qi) : nullptr;
     float *ri = il ? ws_f(ws, wl.ri) : fuse ? qi : nullptr;
-    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[fuse ? 2 : 1]), o->p1, y, o->r, y_sketched},
-                    {ws_f(ws, wl.pack[2]), ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
+    FwdJob fj[2] = {{ws_f(ws, wl.pack[0]), one ? nullptr : ws_f(ws, wl.pack[fuse ? 2 : 1]), o->p1, y, o->r,
+                     y_sketched},
+                    {ws_f(ws, wl.pack[2]), one ? nullptr : ws_f(ws, wl.pack[3]), o->p2, nullptr, nullptr}};
     FwdMc mcr{ws_f(ws, wl.mcpart), ctr, o->mc};
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, fj, 2, B, idx, m, idx_stride, scr, s, &mcr, fuse));

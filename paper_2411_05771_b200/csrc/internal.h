@@ -103,6 +103,8 @@ cudaError_t launch_rotate_adj(const skei_plan *plan, const float *y, float *out,
 // one group (the job-fused packed layout of launch_rotate_pack; jobs[0].xr / xc point to it).
 // Job 0 may fuse the MC residual: y != NULL -> r = p - y_S (if r != NULL) and mc = sum r^2.
 struct FwdJob {
+    // row- / column-packed copies; xc == NULL (groups of 4 only): the column class is staged
+    // from xr through a transposing tensor map (radon_fwd.cu, FwdArgs::tm_col)
     const float *xr, *xc;
     float *p;
     const float *y;  // full sinogram [B][n_full][n_det] or NULL (job 0 only)

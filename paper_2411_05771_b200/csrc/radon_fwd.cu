@@ -54,6 +54,9 @@
 //     r = p - y_S and per-unit partial sums of r^2, summed in a fixed order by the last CTA
 //     to finish (completion counter).  A split unit's pieces go to L2 slots and the last
 //     piece to arrive adds them in CTA order (deterministic, no float atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <type_traits>
 
@@ -99,13 +102,24 @@ constexpr int kAhead = SKEI_FWD_AHEAD;  // pixel loads issued this many lines ah
 #ifndef SKEI_FWD_WHOLE
 #define SKEI_FWD_WHOLE 1  // whole units per CTA when there are 0.9 - 1 units per CTA (A/B knob)
 #endif
+#ifndef SKEI_FWD_WCOST
+#define SKEI_FWD_WCOST 1  // task costs weighted by the angle's expected per-line work (A/B knob)
+#endif
+#ifndef SKEI_FWD_WT_CAND
+#define SKEI_FWD_WT_CAND 10.0
+#endif
+#ifndef SKEI_FWD_WT_WIDE
+#define SKEI_FWD_WT_WIDE 6.0
+#endif
+constexpr double kWtBase = 31.0, kWtCand = SKEI_FWD_WT_CAND, kWtWide = SKEI_FWD_WT_WIDE;
 #ifndef SKEI_FWD_WIDE_SPLIT
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
 constexpr int kCand = 5;    // candidate pixels of a bin pair per line
 constexpr int kPadL = 5;    // zero pixel columns left of the line data (candidates from -5)
-constexpr int kPadR = 5;    // ... and right of it (candidates reach n + 4)
+constexpr int kPadR = 8;    // ... and right of it (candidates reach n + 4; a column block
+                            // staged from the row-packed copy spans R ceil(n / R) <= n + 7)
 constexpr int kColF = 32;   // floats per staged pixel column (R * BB)
 
 struct FwdArgs {
@@ -130,6 +144,13 @@ struct FwdArgs {
     unsigned *queue;  // piece counters of the stream-K split units, indexed by the unit's
                       // first CTA (< gridDim.x; zero before the launch, self-resetting)
     float *scratch;   // split-unit pieces [gridDim.x][2][K * n_det * BB]
+    // tm_col (groups of 4, job.xc == NULL): the column class is staged from the ROW-packed
+    // copy through job j's 4-D tensor map tm[j] — dims (image 4, column n, line 8, row block
+    // nq nblk), byte strides (128, 16, 128 n) — whose box (4, 8, 8, nblk) lands in shared
+    // memory as [row][column][image], the column-packed block (a transposing copy: 16-byte
+    // runs), so rotate + pack writes one packed copy per image instead of two
+    int tm_col;
+    CUtensorMap tm[2];
 };
 
 // One packed block (n pixel columns of 128 B) -> the interior of a staging buffer.
@@ -233,7 +254,7 @@ __device__ __forceinline__ UnitId decode_unit(const Units &U, int nq, int K, int
 }
 
 template <int BB, bool FUSED>
-__global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant__ FwdArgs a) {
     constexpr int R = kColF / BB;
     constexpr int kMaxT = max_tasks<BB>();
     extern __shared__ __align__(128) float smem_raw[];
@@ -248,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     // 5|b| - 2; [2].x Pj (all fp32)
     __shared__ float4 sAngT[kKMax][3];
     __shared__ int sSlot[kKMax];
+    __shared__ int sWt[kKMax];  // per unit angle: cost weight of one (task, block) pair
     __shared__ int sCount;
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
     __shared__ float s_red[kWarps][BB];
@@ -346,7 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
         unit_blocks(u, lo, hi);
         G += hi - lo;
     }
-    auto block_src = [&](int g) -> const float * {
+    // stage block g of this CTA's stream into buffer b: one bulk copy of the packed block, or
+    // (tm_col, column class) one transposing tensor-map box from the row-packed copy
+    auto issue = [&](int g, int b) {
         for (int u = u_first;; ++u) {
             int lo, hi;
             unit_blocks(u, lo, hi);
@@ -354,7 +378,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const UnitId d = decode_unit(U, nq, K, u);
                 const FwdJob &jb = d.job ? a.job[1] : a.job[0];
                 SKEI_DCHECK(d.q < nq && lo + g < a.nblk && d.job < a.njobs, "forward block source");
-                return (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + lo + g) * n * kColF;
+                float *dst = smem + b * stage_f + kPadL * kColF;
+                if (d.cls == 1 && a.tm_col) {
+                    mbar_expect_tx(&full[b], (unsigned)(a.nblk * R * kColF * sizeof(float)));
+                    tma_load_4d(dst, &a.tm[d.job], 0, (lo + g) * R, 0, d.q * a.nblk, &full[b]);
+                } else {
+                    issue_block(dst, (d.cls ? jb.xc : jb.xr) + ((long)d.q * a.nblk + lo + g) * n * kColF, n,
+                                &full[b]);
+                }
+                return;
             }
             g -= hi - lo;
         }
@@ -363,9 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
     // block g + nbuf by the last warp to finish block g (shared counter), so warps are not
     // barrier-synchronised per block and the stream runs on across unit boundaries.
     const int nbuf = max(1, min(a.nbuf, G));
-    if (threadIdx.x == 0)
-        for (int g = 0; g < nbuf && g < G; ++g)
-            issue_block(smem + g * stage_f + kPadL * kColF, block_src(g), n, &full[g]);
+    if (threadIdx.x == 0) {
+        fence_proxy_async();  // the zeroed pads (a tensor-map box may rewrite some, as zeros)
+        for (int g = 0; g < nbuf && g < G; ++g) issue(g, g);
+    }
 
     // this lane's line order: the s-th line visited is l = lane' ^ gray(s) (lane' = lane mod R,
     // gray(s) = s ^ (s >> 1)), so the 32 / BB lanes of one shared-memory phase read R distinct
@@ -462,6 +495,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                                          (float)fmin(Pj, 0.0));
                 sAngT[lane][1] = make_float4((float)(2.0 * ab - 1.0), (float)(3.0 * ab - 2.0),
                                           (float)(4.0 * ab - 2.0), (float)(5.0 * ab - 2.0));
+                // the task's cost per block: a line issues ~kWtBase instructions plus ~kWtCand
+                // per expected extra candidate (c3 is loaded where phi > 4 - 3/|b|, c4 where
+                // phi > 5 - 3/|b|, phi uniform), plus the wide loop's fixed extra
+                const double p3 = 1.0 - fmin(fmax(4.0 - 3.0 / ab, 0.0), 1.0);
+                const double p4 = 1.0 - fmin(fmax(5.0 - 3.0 / ab, 0.0), 1.0);
+                sWt[lane] = SKEI_FWD_WCOST
+                                ? (int)(16.0 * (kWtBase + kWtCand * (p3 + p4) + (4.0 * ab - 1.0 < 2.0 ? kWtWide : 0.0)) /
+                                        kWtBase + 0.5)
+                                : 1;
             }
         }
         for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads) s_cost[tau] = 0;
@@ -491,7 +533,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
             // the chunks c with 64 c <= jh and 64 c + 63 >= jl touch this block
             const int clo = ent.z <= 0 ? 0 : ent.z / kChunk;
             const int chi = ent.w < 0 ? -1 : min(a.chunks - 1, ent.w / kChunk);
-            for (int c = clo; c <= chi; ++c) atomicAdd(&s_cost[k * a.chunks + c], 1);
+            const int wt = sWt[k];
+            for (int c = clo; c <= chi; ++c) atomicAdd(&s_cost[k * a.chunks + c], wt);
         }
 
         // ---- 3. tasks: (angle k, 64-bin chunk) pairs.  A warp runs a task's whole line loop
@@ -723,8 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(FwdArgs a) {
                 const int old = atomicAdd(&done[cb], 1);
                 if (old == kWarps * (g / nbuf + 1) - 1 && g + nbuf < G) {
                     fence_proxy_async();  // generic-proxy reads -> async-proxy writes
-                    issue_block(smem + cb * stage_f + kPadL * kColF, block_src(g + nbuf), n,
-                                &full[cb]);
+                    issue(g + nbuf, cb);
                 }
             }
         }
@@ -1011,7 +1053,11 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
-    const size_t limit = 212 * 1024;  // dynamic shared memory budget (static tables ~11 KB)
+    // dynamic shared memory budget: 227 KB per CTA less the static tables
+    cudaFuncAttributes fa;
+    cudaError_t e0 = cudaFuncGetAttributes(&fa, k_radon_fwd<BB, FUSED>);
+    if (e0 != cudaSuccess) return e0;
+    const size_t limit = (size_t)227 * 1024 - fa.sharedSizeBytes;
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
     const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
@@ -1033,6 +1079,35 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     e = cudaLaunchKernelEx(&cfg, k_radon_fwd<BB, FUSED>, a);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+// The driver's tensor-map encoder, through the runtime's entry-point query (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// the column-class tensor map of a row-packed copy (groups of 4; see FwdArgs::tm_col)
+cudaError_t col_tensor_map(CUtensorMap *tm, const float *xr, int n, int nq) {
+    const auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    const int nblk = (n + 7) / 8;
+    if (nblk > 256) return cudaErrorInvalidValue;  // box dimensions are <= 256
+    cuuint64_t dims[4] = {4, (cuuint64_t)n, 8, (cuuint64_t)nq * nblk};
+    cuuint64_t strides[3] = {128, 16, (cuuint64_t)n * 128};
+    cuuint32_t box[4] = {4, 8, 8, (cuuint32_t)nblk};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(xr), dims, strides, box,
+                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -1057,7 +1132,7 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
                              const int32_t *idx, int m, int idx_stride, const FwdScratch &scr,
                              cudaStream_t s, const FwdMc *mc, bool fused) {
     if (fused && njobs != 2) return cudaErrorInvalidValue;
-    FwdArgs a;
+    FwdArgs a = {};
     a.fused = fused ? 1 : 0;
     a.queue = scr.queue;
     a.scratch = scr.part;
@@ -1075,6 +1150,21 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.g = geom_of(plan);
     a.chunks = (plan->n_det + kChunk - 1) / kChunk;
     if (!mc) a.job[0].y = nullptr;
+    // column class from the row-packed copy (jobs without a column-packed copy): groups of 4
+    a.tm_col = 0;
+    const int njob = fused ? 1 : njobs;
+    const bool no_xc = !jobs[0].xc || (njob > 1 && !jobs[1].xc);
+    if (no_xc) {
+        if (fused || fwd_bb(B, idx_stride) != 4 || !jobs[0].xr) return cudaErrorInvalidValue;
+        if (njob > 1 && (jobs[1].xc || !jobs[1].xr)) return cudaErrorInvalidValue;
+        if (jobs[0].xc) return cudaErrorInvalidValue;
+        for (int j = 0; j < njob; ++j) {
+            const cudaError_t e = col_tensor_map(&a.tm[j], jobs[j].xr, plan->n, B / 4);
+            if (e != cudaSuccess) return e;
+        }
+        if (njob == 1) a.tm[1] = a.tm[0];
+        a.tm_col = 1;
+    }
     if (fused) return launch_bb<2, true>(a, plan->num_sms, s);
     const int bb = fwd_bb(B, idx_stride);
     switch (bb) {

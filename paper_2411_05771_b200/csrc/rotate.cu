@@ -103,18 +103,29 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
         const float cmn = o.fc + fminf(0.f, e * o.cg) + fminf(0.f, -e * o.sg);
         const float rmn = o.fr + fminf(0.f, e * o.sg) + fminf(0.f, e * o.cg);
         const int clo = o.bc + (int)floorf(cmn) - 1, rlo = o.br + (int)floorf(rmn) - 1;
-        for (int it = threadIdx.x; it < kSrc * kSrc; it += kThreads) {
+        // every load of the footprint is issued before the first store (9 x 4 in flight per
+        // thread instead of 4: the loop was 9 serialised DRAM round trips)
+        constexpr int kIt = (kSrc * kSrc + kThreads - 1) / kThreads;
+        float4 t[kIt];
+#pragma unroll
+        for (int q = 0; q < kIt; ++q) {
+            const int it = threadIdx.x + q * kThreads;
             const int i = it / kSrc, j = it - i * kSrc;
             const int r = rlo + i, c = clo + j;
-            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (r >= 0 && r < n && c >= 0 && c < n) {
+            t[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (it < kSrc * kSrc && r >= 0 && r < n && c >= 0 && c < n) {
                 const float *xp = job.x + (long)b0 * nn + (long)r * n + c;
-                t.x = __ldg(xp);
-                if (b0 + 1 < a.B) t.y = __ldg(xp + nn);
-                if (b0 + 2 < a.B) t.z = __ldg(xp + 2 * nn);
-                if (b0 + 3 < a.B) t.w = __ldg(xp + 3 * nn);
+                t[q].x = __ldg(xp);
+                if (b0 + 1 < a.B) t[q].y = __ldg(xp + nn);
+                if (b0 + 2 < a.B) t[q].z = __ldg(xp + 2 * nn);
+                if (b0 + 3 < a.B) t[q].w = __ldg(xp + 3 * nn);
             }
-            *reinterpret_cast<float4 *>(smraw + (i * kSrcPitch + j) * 4) = t;
+        }
+#pragma unroll
+        for (int q = 0; q < kIt; ++q) {
+            const int it = threadIdx.x + q * kThreads;
+            const int i = it / kSrc, j = it - i * kSrc;
+            if (it < kSrc * kSrc) *reinterpret_cast<float4 *>(smraw + (i * kSrcPitch + j) * 4) = t[q];
         }
         __syncthreads();
         float4 res[kT / 8];
@@ -155,6 +166,24 @@ __global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
 #pragma unroll
         for (int i = 0; i < kT / 8; ++i)
             *reinterpret_cast<float4 *>(tile + (tr + 8 * i) * kRow + tc * BB) = res[i];
+    } else if (job.g == nullptr && !XM) {
+        // identity (pack x1): all 4 x BB loads in flight before the tile stores
+        float v[kT / 8][BB];
+#pragma unroll
+        for (int i = 0; i < kT / 8; ++i) {
+            const int r = r0 + tr + 8 * i, c = c0 + tc;
+#pragma unroll
+            for (int b = 0; b < BB; ++b)
+                v[i][b] = (r < n && c < n && b0 + b < a.B) ? __ldg(job.x + (b0 + b) * nn + (long)r * n + c) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kT / 8; ++i) {
+            V t;
+            float *tp = reinterpret_cast<float *>(&t);
+#pragma unroll
+            for (int b = 0; b < BB; ++b) tp[b] = v[i][b];
+            *reinterpret_cast<V *>(tile + (tr + 8 * i) * kRow + tc * BB) = t;
+        }
     } else {
 #pragma unroll
     for (int i = 0; i < kT / 8; ++i) {

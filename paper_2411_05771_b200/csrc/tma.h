@@ -33,6 +33,15 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
             "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// cp.async.bulk.tensor (4-D tiled box of a tensor map in param / const / global space) -> shared
+__device__ __forceinline__ void tma_load_4d(void *dst, const void *tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+    SKEI_DCHECK((smem_u32(dst) & 127u) == 0u, "tensor copy alignment");
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::
+            "r"(smem_u32(dst)), "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
 #ifdef SKEI_CHECKS
     // checked build: a phase that never completes (a lost or mis-sized copy, a missing
