@@ -102,6 +102,11 @@ WsLayout ws_layout(const skei_plan *plan, int B, int m) {
     return w;
 }
 inline float *ws_f(void *ws, size_t off) { return reinterpret_cast<float *>((char *)ws + off); }
+// the column-packed copy's workspace slot, or NULL where the forward stages the column class
+// from the row-packed copy (groups of 4; radon_fwd.cu, tm_col)
+inline float *xc_slot(void *ws, size_t off, int B, int idx_stride) {
+    return (SKEI_PACK_ONE && fwd_bb(B, idx_stride) == 4) ? nullptr : ws_f(ws, off);
+}
 
 skei_status check_idx_args(const skei_plan *plan, int B, const int32_t *idx, int m,
                            int idx_stride) {
@@ -317,9 +322,10 @@ skei_status skei_radon_fwd(const skei_plan *plan, const float *x, float *p, int3
     const WsLayout w = ws_layout(plan, B, m);
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
-    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+    float *xc = xc_slot(ws, w.pack[1], B, idx_stride);
+    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), xc, ctr};
     SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
-    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), p, nullptr, nullptr};
+    FwdJob job{ws_f(ws, w.pack[0]), xc, p, nullptr, nullptr};
     const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, scr, s));
     return SKEI_OK;
@@ -379,11 +385,12 @@ skei_status skei_ei_grad(const skei_plan *plan, int32_t B, const float *x2, cons
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, wl.ctr));
     // d = 2 (x2 - x3), packed for the forward projector (pack[0..1]) and written (pack[2])
     float *d = ws_f(ws, wl.pack[2]), *u = ws_f(ws, wl.pack[3]);
-    RotPackJob pj{x2, d, nullptr, 0, ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), ctr, x3, 2.0f};
+    float *xc = xc_slot(ws, wl.pack[1], B, idx_stride);
+    RotPackJob pj{x2, d, nullptr, 0, ws_f(ws, wl.pack[0]), xc, ctr, x3, 2.0f};
     SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
     // M d = (pi/2m) A_S^T ramp(A_S d); u = d - M d
     float *p = ws_f(ws, wl.ri);  // A_S d (the interleaved-r region is free outside the pass)
-    FwdJob fj{ws_f(ws, wl.pack[0]), ws_f(ws, wl.pack[1]), p, nullptr, nullptr};
+    FwdJob fj{ws_f(ws, wl.pack[0]), xc, p, nullptr, nullptr};
     const FwdScratch scr{ctr + 2, ws_f(ws, wl.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, &fj, 1, B, idx, m, idx_stride, scr, s));
     const bool il = fwd_bb(B, idx_stride) == 4 && pick_bb(B, idx_stride) == 4;
@@ -442,12 +449,21 @@ skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_
     SKEI_CUDA(launch_sumsq(v, B, per, npart, s));
     SKEI_CUDA(launch_normalise(v, v, B, per, npart, nullptr, plan->num_sms, s));
     const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
+    // the packed layout follows each forward's image grouping: per-image sketches (B even)
+    // group differently from the shared full angle set, so v is packed again for A_S v
+    const bool repack = fwd_bb(B, idx_stride) != fwd_bb(B, 0);
     for (int it = 0; it < iters; ++it) {
-        RotPackJob pj{v, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+        float *xc = xc_slot(ws, w.pack[1], B, 0);
+        RotPackJob pj{v, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), xc, ctr};
         SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, 0), s));
-        FwdJob ff{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), pf, nullptr, nullptr};
+        FwdJob ff{ws_f(ws, w.pack[0]), xc, pf, nullptr, nullptr};
         SKEI_CUDA(launch_radon_fwd(plan, &ff, 1, B, all, nf, 0, scr, s));   // A v
-        FwdJob fs{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ps, nullptr, nullptr};
+        if (repack) {
+            xc = xc_slot(ws, w.pack[1], B, idx_stride);
+            RotPackJob ps_{v, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), xc, ctr};
+            SKEI_CUDA(launch_rotate_pack(plan, &ps_, 1, B, fwd_bb(B, idx_stride), s));
+        }
+        FwdJob fs{ws_f(ws, w.pack[0]), xc, ps, nullptr, nullptr};
         SKEI_CUDA(launch_radon_fwd(plan, &fs, 1, B, idx, m, idx_stride, scr, s));  // A_S v
         AdjJob a1{pf, u, -1.0f};  // u = -A^T A v
         SKEI_CUDA(launch_radon_adj(plan, &a1, 1, B, all, nf, 0, s));
@@ -494,10 +510,11 @@ skei_status skei_fbp_adjoint(const skei_plan *plan, const float *x, float *p, in
     const WsLayout w = ws_layout(plan, B, m);
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *ctr = reinterpret_cast<unsigned *>(ws_f(ws, w.ctr));
-    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ctr};
+    float *xc = xc_slot(ws, w.pack[1], B, idx_stride);
+    RotPackJob pj{x, nullptr, nullptr, 0, ws_f(ws, w.pack[0]), xc, ctr};
     SKEI_CUDA(launch_rotate_pack(plan, &pj, 1, B, fwd_bb(B, idx_stride), s));
     float *ax = ws_f(ws, w.q);  // A_S x
-    FwdJob job{ws_f(ws, w.pack[0]), ws_f(ws, w.pack[1]), ax, nullptr, nullptr};
+    FwdJob job{ws_f(ws, w.pack[0]), xc, ax, nullptr, nullptr};
     const FwdScratch scr{ctr + 2, ws_f(ws, w.fscr)};
     SKEI_CUDA(launch_radon_fwd(plan, &job, 1, B, idx, m, idx_stride, scr, s));
     // p = (pi / 2 m_total) ramp(A_S x): the scale folded into the ramp's spectrum

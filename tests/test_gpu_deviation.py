@@ -42,6 +42,29 @@ def test_sketch_deviation_one_application_matches_oracle(name):
         assert abs(float(lam[b]) - ref_lam) <= 1e-4 * ref_lam, (b, float(lam[b]), ref_lam)
 
 
+@pytest.mark.parametrize("name,per_image", [("cfg1", True), ("cfg2", True), ("cfg2", False)])
+def test_sketch_deviation_batch_of_four(name, per_image):
+    """B = 4 start images: the full-angle forward runs on groups of 4 (one packed copy, the
+    column class through the tensor map); with per-image sketches (idx_stride = m) the
+    sketched forward groups images singly, so v is packed again in that layout.  One
+    application of D against the oracle with each image's own sketch."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    idxs = [np.asarray(sk.draw(0, 1, b if per_image else sk.SHARED_IMAGE, cfg.n_full, cfg.m)[1])
+            for b in range(4)]
+    idx = np.stack(idxs) if per_image else idxs[0][None]
+    v0 = np.random.default_rng(5).standard_normal((4, cfg.N, cfg.N)).astype(np.float32)
+    v = dev(v0)
+    lam = sk.sketch_deviation(plan, idx_t(idx), v, 1)
+    dv = (v.double() * lam.double()[:, None, None]).cpu().numpy()
+    for b in range(4):
+        ref_lam, ref_v = oracle.sketch_deviation(v0[b], idxs[b], cfg.n_full, cfg.n_det, 1)
+        ref = ref_v * ref_lam
+        err = np.abs(dv[b] - ref).max()
+        assert err <= 1e-4 * np.abs(ref).max(), (b, err, np.abs(ref).max())
+        assert abs(float(lam[b]) - ref_lam) <= 1e-4 * ref_lam, (b, float(lam[b]), ref_lam)
+
+
 @pytest.mark.parametrize("name,iters", [("cfg1", 80), ("cfg2", 30)])
 def test_sketch_deviation_power_iteration_tracks_oracle(name, iters):
     """The converged estimate: both power iterations from the same start image approach
