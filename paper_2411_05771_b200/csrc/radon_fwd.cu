@@ -116,6 +116,10 @@ constexpr double kWtBase = 31.0, kWtCand = SKEI_FWD_WT_CAND, kWtWide = SKEI_FWD_
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
+constexpr int kMaxBand = 64;     // band angles of the source class considered for a move
+#ifndef SKEI_FWD_BAND
+#define SKEI_FWD_BAND 1  // flexible class band near the diagonals (A/B knob)
+#endif
 constexpr int kCand = 5;    // candidate pixels of a bin pair per line
 constexpr int kPadL = 5;    // zero pixel columns left of the line data (candidates from -5)
 constexpr int kPadR = 8;    // ... and right of it (candidates reach n + 4; a column block
@@ -141,6 +145,11 @@ struct FwdArgs {
     int mc_slots;
     unsigned *mc_ctr;
     float *mc_out;
+    // flexible class band (shared sketches; 0 = off): angles within `band` index units of a
+    // diagonal (|4 i - n_full| or |4 i - 3 n_full| <= band, i.e. min(|cos|, |sin|) >= 0.68)
+    // are exact in either class (the line loop holds for |beta| >= 2/3), so a few of them may
+    // change class to make the class sizes multiples of K (fewer, whole units)
+    int band;
     unsigned *queue;  // piece counters of the stream-K split units, indexed by the unit's
                       // first CTA (< gridDim.x; zero before the launch, self-resetting)
     float *scratch;   // split-unit pieces [gridDim.x][2][K * n_det * BB]
@@ -272,6 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
     __shared__ int sWt[kKMax];  // per unit angle: cost weight of one (task, block) pair
     __shared__ int sCount;
     __shared__ int s_uoff[kMaxQ + 1], s_nrow[kMaxQ];
+    __shared__ int s_mv[3];           // class band moves: shift (+: col -> row), key bound (D, I)
+    __shared__ int s_bkey[kMaxBand];  // the source side's band angles, key = (dist << 16) | index
     __shared__ float s_red[kWarps][BB];
     __shared__ bool s_last;
     __shared__ int4 s_task[kWarps * kMaxT];  // per task: angle slot, chunk bin, chunk Pj split
@@ -290,17 +301,85 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                     nq <= kMaxQ,
                 "forward scratch / piece / table sizes");
 
-    // ---- 1. class sizes per image group -> unit table (identical in every CTA)
+    // ---- 1. the class rule and the class sizes per image group -> unit table (identical in
+    // every CTA).  Strict rule: row class iff |cos| >= |sin| (4 i <= n_full or 4 i >= 3 n_full).
+    // With a flexible band (shared sketch): the shift s in [-a, b] (a / b: band angles strictly
+    // in the row / column class) that minimises ceil(n_row / K) + ceil(n_col / K), smallest |s|
+    // first; the |s| band angles nearest a diagonal (key (distance, index)) change class.
+    auto strict_row = [&](int i) { return (4 * i <= n_full) || (4 * i >= 3 * n_full); };
+    auto diag_dist = [&](int i) { return min(abs(4 * i - n_full), abs(4 * i - 3 * n_full)); };
+    if (warp == 0) {
+        int nr0 = 0, na = 0, nb = 0;
+        if (a.band > 0) {
+            for (int base = 0; base < a.m; base += 32) {
+                const int k = base + lane;
+                bool r = false, ba = false, bb = false;
+                if (k < a.m) {
+                    const int i = a.idx[k];
+                    r = strict_row(i);
+                    const bool bd = diag_dist(i) <= a.band;
+                    ba = bd && r;
+                    bb = bd && !r;
+                }
+                nr0 += __popc(__ballot_sync(0xffffffffu, r));
+                na += __popc(__ballot_sync(0xffffffffu, ba));
+                nb += __popc(__ballot_sync(0xffffffffu, bb));
+            }
+        }
+        int sh = 0;
+        if (a.band > 0) {
+            auto units_of = [&](int nr) { return (nr + K - 1) / K + (a.m - nr + K - 1) / K; };
+            int best = units_of(nr0);
+            for (int t = 1; t <= max(na, nb); ++t) {
+                if (t <= na && units_of(nr0 - t) < best) { best = units_of(nr0 - t); sh = -t; }
+                if (t <= nb && units_of(nr0 + t) < best) { best = units_of(nr0 + t); sh = t; }
+            }
+            sh = max(-kMaxBand, min(kMaxBand, sh));
+        }
+        int nsrc = 0;  // the source side's band angles -> s_bkey
+        if (sh != 0) {
+            for (int base = 0; base < a.m; base += 32) {
+                const int k = base + lane;
+                bool src = false;
+                int key = 0;
+                if (k < a.m) {
+                    const int i = a.idx[k];
+                    src = diag_dist(i) <= a.band && (sh < 0) == strict_row(i);
+                    key = (diag_dist(i) << 16) | i;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, src);
+                const int pre = nsrc + __popc(bal & ((1u << lane) - 1u));
+                if (src && pre < kMaxBand) s_bkey[pre] = key;
+                nsrc += __popc(bal);
+            }
+            nsrc = min(nsrc, kMaxBand);
+            __syncwarp();
+            for (int e = lane; e < nsrc; e += 32) {  // the |s|-th smallest key bounds the moves
+                const int key = s_bkey[e];
+                int rk = 0;
+                for (int o = 0; o < nsrc; ++o) rk += s_bkey[o] < key;
+                if (rk == abs(sh) - 1) s_mv[1] = key;
+            }
+        }
+        if (lane == 0) {
+            s_mv[0] = sh;
+            if (sh == 0) s_mv[1] = -1;
+        }
+    }
+    __syncthreads();
+    const int mv_sh = s_mv[0], mv_key = s_mv[1];
+    auto is_row = [&](int i) -> bool {
+        const bool st = strict_row(i);
+        if (mv_sh == 0 || diag_dist(i) > a.band || (mv_sh < 0) != st) return st;
+        return ((diag_dist(i) << 16) | i) <= mv_key ? !st : st;
+    };
     for (int q = warp; q < nq; q += kWarps) {
         const int32_t *iq = a.idx + (a.idx_stride ? (long)q * (FUSED ? 1 : BB) * a.idx_stride : 0);
         int cnt = 0;
         for (int base = 0; base < a.m; base += 32) {
             const int k = base + lane;
             bool row = false;
-            if (k < a.m) {
-                const int i = iq[k];
-                row = (4 * i <= n_full) || (4 * i >= 3 * n_full);
-            }
+            if (k < a.m) row = is_row(iq[k]);
             cnt += __popc(__ballot_sync(0xffffffffu, row));
         }
         if (lane == 0) s_nrow[q] = cnt;
@@ -452,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 bool in = false;
                 if (k < a.m) {
                     const int i = idx[k];
-                    const bool row_class = (4 * i <= n_full) || (4 * i >= 3 * n_full);
+                    const bool row_class = is_row(i);
                     in = (d.cls == 0) ? row_class : !row_class;
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
@@ -921,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 bool in = false;
                 if (k < a.m) {
                     const int i = idx[k];
-                    const bool row_class = (4 * i <= n_full) || (4 * i >= 3 * n_full);
+                    const bool row_class = is_row(i);
                     in = (d.cls == 0) ? row_class : !row_class;
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, in);
@@ -1149,6 +1228,10 @@ cudaError_t launch_radon_fwd(const skei_plan *plan, const FwdJob *jobs, int njob
     a.B = B;
     a.g = geom_of(plan);
     a.chunks = (plan->n_det + kChunk - 1) / kChunk;
+    // band: |4 i - n_full| pi / (4 n_full) <= acos(0.68) - pi / 4 keeps min(|cos|, |sin|) >= 0.68
+    a.band = (SKEI_FWD_BAND && idx_stride == 0)
+                 ? (int)floor((acos(0.68) - M_PI / 4) * 4.0 * plan->n_full / M_PI)
+                 : 0;
     if (!mc) a.job[0].y = nullptr;
     // column class from the row-packed copy (jobs without a column-packed copy): groups of 4
     a.tm_col = 0;

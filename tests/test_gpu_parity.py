@@ -248,6 +248,37 @@ def test_pass_parity_full_size_class_boundary_angles(g):
             assert abs(float(out[k][b]) - ref[k]) <= TOL * abs(ref[k]), (k, b)
 
 
+def _band_sketch(n_full, n_row, seed):
+    """m = 90 angles of n_full = 360 with n_row of them strictly in the row class (|cos| >=
+    |sin|), including band angles (within 2.1 degrees of 45 / 135 degrees) on both sides."""
+    rng = np.random.default_rng(seed)
+    strict_row = lambda i: 4 * i <= n_full or 4 * i >= 3 * n_full  # noqa: E731
+    rows = [i for i in range(n_full) if strict_row(i)]
+    cols = [i for i in range(n_full) if not strict_row(i)]
+    must_r, must_c = [88, 89, 90, 270, 271], [91, 92, 268, 269]
+    r = must_r + list(rng.choice([i for i in rows if i not in must_r], n_row - len(must_r), replace=False))
+    c = must_c + list(rng.choice([i for i in cols if i not in must_c], 90 - n_row - len(must_c), replace=False))
+    return np.array(sorted(r + c), np.int32)
+
+
+@pytest.mark.parametrize("n_row", [46, 44, 43, 47])
+def test_radon_fwd_flexible_class_band(n_row):
+    """cfg3 geometry (K = 5 angles per unit) with n_row strict row-class angles: the forward
+    moves the band angles nearest a diagonal to the other class so the class sizes become
+    multiples of K (46 -> 45, 44 -> 45, 43 -> 45, 47 -> 45): those angles are projected with
+    |beta| in [0.68, 1/sqrt 2) — still exact for the bin-pair line loop — against the
+    oracle, for one group of 4 images (one packed copy, tensor-map columns) and singly."""
+    cfg = synth.CONFIGS["cfg3"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    idx = _band_sketch(cfg.n_full, n_row, n_row)
+    x = synth.rand_images(4, cfg.N, 21)
+    p = sk.radon_fwd(plan, dev(x), idx_t(idx[None]))
+    for b in range(4):
+        close(p[b], oracle.fwd(x[b], idx, cfg.n_full, cfg.n_det), f"band fwd n_row={n_row} b={b}")
+    p1 = sk.radon_fwd(plan, dev(x[:1]), idx_t(idx[None]))
+    close(p1[0], oracle.fwd(x[0], idx, cfg.n_full, cfg.n_det), f"band fwd single n_row={n_row}")
+
+
 def test_quad_backprojector_ragged_tiles_all_patterns():
     """The quad backprojector (32 x 32 tiles, four pixels per thread; chosen when its grid
     fills a wave) at N = 500 — ragged last tiles in both directions — with a sketch of every
