@@ -58,6 +58,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "internal.h"
@@ -116,6 +117,7 @@ constexpr double kWtBase = 31.0, kWtCand = SKEI_FWD_WT_CAND, kWtWide = SKEI_FWD_
 #define SKEI_FWD_WIDE_SPLIT 1  // compile the line loop with / without the fifth candidate
 #endif
 constexpr int kMaxPieces = 256;  // pieces of one split unit (<= CTAs <= 256)
+constexpr int kMaxDevices = 64;  // devices with cached launch attributes
 constexpr int kMaxBand = 64;     // band angles of the source class considered for a move
 #ifndef SKEI_FWD_BAND
 #define SKEI_FWD_BAND 1  // flexible class band near the diagonals (A/B knob)
@@ -1132,23 +1134,40 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
-    // dynamic shared memory budget: 227 KB per CTA less the static tables
-    cudaFuncAttributes fa;
-    cudaError_t e0 = cudaFuncGetAttributes(&fa, k_radon_fwd<BB, FUSED>);
-    if (e0 != cudaSuccess) return e0;
-    const size_t limit = (size_t)227 * 1024 - fa.sharedSizeBytes;
+    // dynamic shared memory budget: 227 KB per CTA less the static tables.  The function
+    // attributes are set once per device (the launch path stays free of driver queries: it
+    // runs every pass, also on the e2e host path)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    static int limit_of[kMaxDevices];  // 0: not yet set up on that device
+    static std::mutex mu;
+    int limit_i;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (limit_of[dev] == 0) {
+            cudaFuncAttributes fa;
+            e = cudaFuncGetAttributes(&fa, k_radon_fwd<BB, FUSED>);
+            if (e != cudaSuccess) return e;
+            const int lim = 227 * 1024 - (int)fa.sharedSizeBytes;
+            e = cudaFuncSetAttribute(k_radon_fwd<BB, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+            if (e != cudaSuccess) return e;
+            // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared
+            // memory; the split-unit scratch, the piece counters and kMaxPieces assume grid <=
+            // num_sms <= 256)
+            int per_sm = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB, FUSED>, kThreads, lim);
+            if (e != cudaSuccess) return e;
+            if (per_sm < 1) return cudaErrorInvalidConfiguration;
+            limit_of[dev] = lim;
+        }
+        limit_i = limit_of[dev];
+    }
+    const size_t limit = (size_t)limit_i;
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
     const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_radon_fwd<BB, FUSED>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    // persistent grid: one CTA per SM (the kernel needs one SM's registers and shared memory;
-    // the split-unit scratch, the piece counters and kMaxPieces assume grid <= num_sms <= 256)
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_radon_fwd<BB, FUSED>, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
     if (num_sms > kMaxPieces || num_sms > kPassCounters - 2) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)num_sms, 1, 1);
@@ -1173,8 +1192,26 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// the column-class tensor map of a row-packed copy (groups of 4; see FwdArgs::tm_col)
+// the column-class tensor map of a row-packed copy (groups of 4; see FwdArgs::tm_col),
+// from a small cache keyed by (copy, n, groups): the pass reuses its workspace every step
 cudaError_t col_tensor_map(CUtensorMap *tm, const float *xr, int n, int nq) {
+    struct Entry {
+        const float *xr;
+        int n, nq;
+        CUtensorMap tm;
+    };
+    constexpr int kCache = 16;
+    static Entry cache[kCache];
+    static int next = 0;
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (int i = 0; i < kCache; ++i)
+            if (cache[i].xr == xr && cache[i].n == n && cache[i].nq == nq) {
+                *tm = cache[i].tm;
+                return cudaSuccess;
+            }
+    }
     const auto enc = tensor_map_encoder();
     if (!enc) return cudaErrorNotSupported;
     const int nblk = (n + 7) / 8;
@@ -1186,7 +1223,11 @@ cudaError_t col_tensor_map(CUtensorMap *tm, const float *xr, int n, int nq) {
     const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(xr), dims, strides, box,
                            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[next] = Entry{xr, n, nq, *tm};
+    next = (next + 1) % kCache;
+    return cudaSuccess;
 }
 
 }  // namespace
