@@ -93,8 +93,9 @@ const char *skei_last_cuda_error(void);                  /* thread-local, after 
 
 /* Device scratch needed by skei_radon_fwd / skei_fbp / skei_ei_residual / skei_pass
  * for `batch` images and sketch size m (bytes; 256-byte aligned pieces): the filtered
- * sinogram, the residual partial sums and four packed copies of the images (the forward
- * projector's TMA-friendly input layout, ~4 * batch * n^2 floats). */
+ * sinogram, the residual partial sums and slots for four packed copies of the images (the
+ * forward projector's TMA-friendly input layout, ~4 * batch * n^2 floats; groups of 4
+ * images sharing a sketch use two of them, one row-lines copy per image). */
 size_t skei_workspace_bytes(const skei_plan *plan, int32_t batch, int32_t m);
 
 /* ---------------------------------------------------------------- a1: draws --
