@@ -33,6 +33,9 @@ constexpr int kThreads = 256;   // 32 columns x 8 row groups; a thread owns 4 ro
 // pitch (16-byte slots: a quarter-warp's bilinear taps spread over the bank groups)
 constexpr int kSrc = 48, kSrcPitch = 49;
 constexpr int kStageF = kSrc * kSrcPitch * 4;
+#ifndef SKEI_ROT_MINB
+#define SKEI_ROT_MINB 5  // CTAs per SM the rotate + pack kernel's registers must allow (A/B knob)
+#endif
 #ifndef SKEI_ROT_STAGED
 #define SKEI_ROT_STAGED 1  // shared-g rotations of groups of 4 via the staged footprint (A/B knob)
 #endif
@@ -52,7 +55,7 @@ template <> struct VecT<4> { using T = float4; };
 // XM: the identity job packs ascale * (x - xm) (a separate instantiation, so the pass's
 // rotation + packing is compiled without it)
 template <int BB, bool XM>
-__global__ void __launch_bounds__(kThreads) k_rotate_pack(RotPackArgs a) {
+__global__ void __launch_bounds__(kThreads, SKEI_ROT_MINB) k_rotate_pack(RotPackArgs a) {
     constexpr int R = 32 / BB;
     using V = typename VecT<BB>::T;
     constexpr int kRow = kT * BB + 4;  // padded tile row (floats)
