@@ -879,9 +879,11 @@ def main():
     achieved = 4.0 * fwd_taps / (float(fwd_ms.mean()) * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # the capture's per-launch DRAM bytes, for the config it was taken on
         try:
-            traffic = json.load(open(tf)).get(dname)
+            tj = json.load(open(tf))
+            if tj.get("config", "cfg3") == args.config and getattr(args, "mode", None) in (None, "uniform"):
+                traffic = tj.get(dname)
         except Exception:
             traffic = None
     hbm_gbs, hbm_src = hbm_peak()
