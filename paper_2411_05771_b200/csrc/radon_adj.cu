@@ -392,6 +392,9 @@ constexpr int kQKC = 12;     // angles per staged chunk
 #ifndef SKEI_ADJQ_FUSED
 #define SKEI_ADJQ_FUSED 1    // job-fused groups use the quad kernel (A/B knob)
 #endif
+#ifndef SKEI_ADJQ_NOBAR
+#define SKEI_ADJQ_NOBAR 1    // quad kernel, bulk + full table: last warp refills, no chunk barrier
+#endif
 #ifndef SKEI_ADJQ_UNROLL
 #define SKEI_ADJQ_UNROLL 1   // angles unrolled in the quad kernel's loop
 #endif
@@ -406,6 +409,7 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
     __shared__ float s_red[kThreads / 32][BB];
     __shared__ bool s_last;
     __shared__ __align__(8) uint64_t full[2];
+    __shared__ unsigned s_done[2];  // warps finished with each buffer (monotonic; SKEI_ADJQ_NOBAR)
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
@@ -430,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
     if (BULK && threadIdx.x == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
+        s_done[0] = s_done[1] = 0u;
         fence_mbar_init();
     }
     const bool full_tab = a.m <= kTab;
@@ -571,9 +576,23 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
                 default: angle(I3{}, std::true_type{}, wb, u, ac); break;
             }
         }
-        __syncthreads();  // buffer bf (and its table) is free for chunk ch + 2
-        if constexpr (BULK) {
-            if (ch + 2 < nchunks) produce(ch + 2, bf);
+        if (BULK && SKEI_ADJQ_NOBAR && full_tab) {
+            // no block-wide barrier per chunk: the last warp out of buffer bf refills it with
+            // chunk ch + 2 (the angle table is complete up front, so a refill is only the bulk
+            // copies), so warps drift up to a chunk apart instead of meeting every 12 angles
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();  // this warp's reads of the buffer are complete
+                const unsigned old = atomicAdd(&s_done[bf], 1u);
+                if (old == (unsigned)(kThreads / 32) * (unsigned)(ch / 2 + 1) - 1u && ch + 2 < nchunks) {
+                    if constexpr (BULK) issue_bulk(ch + 2, bf);
+                }
+            }
+        } else {
+            __syncthreads();  // buffer bf (and its table) is free for chunk ch + 2
+            if constexpr (BULK) {
+                if (ch + 2 < nchunks) produce(ch + 2, bf);
+            }
         }
     }
 
