@@ -382,7 +382,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
 // rows of one quad column (conflict-free, as the pair kernel).  Tile 32 x 32, 256 threads.
 constexpr int kQTileH = 32;  // quad tile height (rows); width kTileW
 constexpr int kQW = 48;      // staged bins per angle (>= 31 sqrt 2 + 4)
-constexpr int kQKC = 12;     // angles per staged chunk
+#ifndef SKEI_ADJQ_KC
+#define SKEI_ADJQ_KC 12
+#endif
+#ifndef SKEI_ADJQ_NB
+#define SKEI_ADJQ_NB 2
+#endif
+constexpr int kQKC = SKEI_ADJQ_KC;  // angles per staged chunk
+constexpr int kQNB = SKEI_ADJQ_NB;  // staged chunks in flight (bulk staging)
 #ifndef SKEI_ADJQ_MINB
 #define SKEI_ADJQ_MINB 3     // CTAs per SM the quad kernel is compiled for
 #endif
@@ -403,13 +410,15 @@ constexpr int kQUnroll = SKEI_ADJQ_UNROLL;
 template <int BB, int NJ, bool BULK, bool FUSED>
 __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_ADJQ_MINB)
     k_radon_adj_quad(AdjArgs a) {
-    __shared__ __align__(128) float win[2][NJ][kQKC * kQW * BB];
+    // window buffers: kQNB with bulk staging (refilled by the last warp out), 2 otherwise
+    constexpr int NB = BULK ? kQNB : 2;
+    __shared__ __align__(128) float win[NB][NJ][kQKC * kQW * BB];
     __shared__ float s_off[kTab], s_cos[kTab], s_sin[kTab];
     __shared__ int s_w0[kTab], s_pat[kTab];
     __shared__ float s_red[kThreads / 32][BB];
     __shared__ bool s_last;
-    __shared__ __align__(8) uint64_t full[2];
-    __shared__ unsigned s_done[2];  // warps finished with each buffer (monotonic; SKEI_ADJQ_NOBAR)
+    __shared__ __align__(8) uint64_t full[NB];
+    __shared__ unsigned s_done[NB];  // warps finished with each buffer (monotonic; SKEI_ADJQ_NOBAR)
 
     const int n = a.g.n, n_det = a.g.n_det;
     const int tile = blockIdx.x;
@@ -432,9 +441,10 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
 
     const int nchunks = (a.m + kQKC - 1) / kQKC;
     if (BULK && threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        s_done[0] = s_done[1] = 0u;
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(&full[i], 1);
+            s_done[i] = 0u;
+        }
         fence_mbar_init();
     }
     const bool full_tab = a.m <= kTab;
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
         const int pat = ac <= (1.f / 3.f) ? 0 : ac <= 0.5f ? 1 : ac <= (2.f / 3.f) ? 2 : 3;
         s_pat[e] = pat | (cf < 0.f ? 4 : 0);
     };
-    auto tbase = [&](int ch) { return full_tab ? ch * kQKC : (ch & 1) * kQKC; };
+    auto tbase = [&](int ch) { return full_tab ? ch * kQKC : (ch % NB) * kQKC; };
     auto table = [&](int ch) {
         const int k0 = ch * kQKC;
         const int kc = min(kQKC, a.m - k0);
@@ -507,8 +517,7 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
         cp_async_commit();
     };
     if constexpr (BULK) {
-        produce(0, 0);
-        if (nchunks > 1) produce(1, 1);
+        for (int c = 0; c < NB && c < nchunks; ++c) produce(c, c);
     } else {
         stage(0, 0);
     }
@@ -536,9 +545,9 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
         }
     };
     for (int ch = 0; ch < nchunks; ++ch) {
-        const int bf = ch & 1;
+        const int bf = ch % NB;
         if constexpr (BULK) {
-            mbar_wait(&full[bf], (unsigned)((ch >> 1) & 1));
+            mbar_wait(&full[bf], (unsigned)((ch / NB) & 1));
         } else {
             if (ch + 1 < nchunks) stage(ch + 1, bf ^ 1);
             if (ch + 1 < nchunks)
@@ -584,14 +593,14 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
             if (lane == 0) {
                 __threadfence_block();  // this warp's reads of the buffer are complete
                 const unsigned old = atomicAdd(&s_done[bf], 1u);
-                if (old == (unsigned)(kThreads / 32) * (unsigned)(ch / 2 + 1) - 1u && ch + 2 < nchunks) {
-                    if constexpr (BULK) issue_bulk(ch + 2, bf);
+                if (old == (unsigned)(kThreads / 32) * (unsigned)(ch / NB + 1) - 1u && ch + NB < nchunks) {
+                    if constexpr (BULK) issue_bulk(ch + NB, bf);
                 }
             }
         } else {
-            __syncthreads();  // buffer bf (and its table) is free for chunk ch + 2
+            __syncthreads();  // buffer bf (and its table) is free for chunk ch + NB
             if constexpr (BULK) {
-                if (ch + 2 < nchunks) produce(ch + 2, bf);
+                if (ch + NB < nchunks) produce(ch + NB, bf);
             }
         }
     }
