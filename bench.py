@@ -126,14 +126,17 @@ def parse():
     ap.add_argument("--impl", default="skei", choices=["skei", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(synth.CONFIGS))
     ap.add_argument("--mode", default="uniform", choices=["uniform", "interleaved"])
-    ap.add_argument("--split", default="batch", choices=["batch", "angle", "angle-ag", "angle-p2p"],
+    ap.add_argument("--split", default="batch", choices=["batch", "angle", "angle-ag", "angle-p2p", "angle-rs"],
                     help="batch: every rank runs its own batch (weak scaling, no collective); "
                          "angle: one batch, the sketch's angles split over the ranks with one "
                          "NCCL all-reduce of the partial backprojections (strong scaling, "
                          "BASELINE cfg5); angle-ag: the same split exchanging filtered "
                          "sinogram rows by all-gather, row-band backprojection (SURVEY 8(f) #2); "
                          "angle-p2p: the same with the exchange fused into the ramp kernel "
-                         "(P2P stores into symmetric memory, no NCCL on the data path)")
+                         "(P2P stores into symmetric memory, no NCCL on the data path); "
+                         "angle-rs: each rank backprojects its own angles and the "
+                         "backprojector's epilogue stores every partial row into its band "
+                         "owner's slot (reduce-scatter fused into the kernel, SURVEY 8(f) #2 (b))")
     ap.add_argument("--path", default="pass", choices=["pass", "ei-grad", "rei", "deviation"],
                     help="pass: the sketched-EI operator pass (the headline); ei-grad: the next "
                          "row, the EI branch's gradient T_g^T (I - M) 2 (x2 - x3) (skei_ei_grad); "
@@ -348,11 +351,13 @@ def run_angle(args):
     mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     split_fn = {"angle-ag": skdist.angle_split_pass_allgather,
-                "angle-p2p": skdist.angle_split_pass_p2p}.get(args.split, skdist.angle_split_pass)
+                "angle-p2p": skdist.angle_split_pass_p2p,
+                "angle-rs": skdist.angle_split_pass_rs}.get(args.split, skdist.angle_split_pass)
 
-    # the P2P split's symmetric-memory buffers are allocated (and rendezvoused) once, outside
+    # the P2P splits' symmetric-memory buffers are allocated (and rendezvoused) once, outside
     # the timed loop
-    p2p = skdist.P2PBuffers(cfg.B, cfg.m, cfg.n_det, dev) if args.split == "angle-p2p" else None
+    p2p = (skdist.P2PBuffers(cfg.B, cfg.m, cfg.n_det, dev) if args.split == "angle-p2p" else
+           skdist.RSBuffers(cfg.B, cfg.N, dev) if args.split == "angle-rs" else None)
 
     def step(it):
         g, idx = sk.draw_device(args.seed, it, 0, 1, True, cfg.n_full, cfg.m, mode)
@@ -392,9 +397,13 @@ def run_angle(args):
                        "parallelism": f"angle split x{world}" + {
                            "angle-ag": " (NCCL all-gather of filtered rows, row-band backprojection)",
                            "angle-p2p": " (filtered rows stored to every rank by the ramp kernel "
-                                        "over NVLink P2P, row-band backprojection)"}.get(args.split, ""),
+                                        "over NVLink P2P, row-band backprojection)",
+                           "angle-rs": " (partial backprojection rows stored to their band owner "
+                                       "by the backprojector over NVLink P2P, fixed-order band "
+                                       "sum)"}.get(args.split, ""),
                        **({"allgather_bytes": int(out["allgather_bytes"])} if args.split == "angle-ag"
                           else {"p2p_bytes": int(out["p2p_bytes"])} if args.split == "angle-p2p"
+                          else {"rs_bytes_per_gpu": int(out["rs_bytes"])} if args.split == "angle-rs"
                           else {"allreduce_bytes": int(out["allreduce_bytes"])}),
                        "launch": "direct (not graphed): library calls + NCCL collectives"},
             "clocks": clk.summary(),
@@ -624,7 +633,7 @@ def main():
         return run_ei_grad(args)
     if args.path == "rei":
         return run_rei(args)
-    if args.split in ("angle", "angle-ag", "angle-p2p"):
+    if args.split in ("angle", "angle-ag", "angle-p2p", "angle-rs"):
         if args.config == "cfg3" and "--config" not in sys.argv:
             args.config = "cfg5"
         return run_angle(args)
@@ -793,7 +802,7 @@ def main():
                               hg=torch.empty(ng, dtype=torch.int32).pin_memory(),
                               hidx=torch.empty(ng, m, dtype=torch.int32).pin_memory(),
                               hmc=torch.empty(B).pin_memory(), hei=torch.empty(B).pin_memory(),
-                              ys=torch.empty(B, m, cfg.n_det).pin_memory() if shared else None,
+                              ys=torch.empty(B, m, cfg.n_det).pin_memory(),
                               hgrad=torch.empty(B, N, N).pin_memory() if args.e2e_grad else None,
                               done=None, fl=torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)))
         results = []
@@ -844,8 +853,8 @@ def main():
                 el = float(t.item())
             reps.append(el)
         el = float(np.median(reps))
-        # a shared sketch copies only y's m sketched rows (skei_pass_host), else all of y
-        y_h2d = B * m * cfg.n_det * 4 if shared else hy.numel() * 4
+        # only each image's m sketched rows of y cross the link (skei_pass_host gathers them)
+        y_h2d = B * m * cfg.n_det * 4
         h2d = hx1.numel() * 4 + y_h2d + ng * 4 + ng * m * 4
         d2h = 2 * B * 4 + (B * N * N * 4 if args.e2e_grad else 0)
         e2e = {"value": passes_per_step * args.steps / el, "unit": UNIT,
@@ -856,7 +865,7 @@ def main():
                           "the gradient back too)",
                "timing": "host wall clock over all steps; per step: host draw, H2D of x1, y_S "
                          "(the sketched rows of y gathered into a pinned staging buffer by the "
-                         "library; all of y for per-image sketches), g, idx "
+                         "library, each image's own rows for per-image sketches), g, idx "
                          "from pinned memory, the pass, D2H of its results, in-stream L2 flush "
                          "(256 MB write) behind it; slots with their own streams rotate, so one "
                          "step's H2D overlaps the previous steps' passes (3 slots); the median "

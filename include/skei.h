@@ -171,6 +171,38 @@ skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float 
                                   float *grad_band, float *ei_band, void *ws, size_t ws_bytes,
                                   skei_stream stream);
 
+/* ---------- next row: the backprojector with its reduce-scatter fused --
+ * The other communication-reduced form of the single-image angle split: each rank
+ * backprojects only its own angle shard — x_fbp partial (pi / 2 m_total) A_{S_r}^T q and
+ * grad partial 2 A_{S_r}^T r (the pass's sums over angles split over ranks, PAPER.md L70,
+ * L92) — and the kernel's epilogue stores every output row straight into the receive
+ * buffer of the rank that owns the row's band (P2P stores over NVLink into symmetric
+ * memory), so the reduce-scatter of 2 B n^2 floats overlaps the backprojection tile by
+ * tile; no NCCL on the data path.  Row bands as dist.batch_range(n, o, world): rank o owns
+ * rows [o q + min(o, n mod world), ... + q + (o < n mod world)), q = n / world; bmax =
+ * ceil(n / world).  Receive buffer of every rank: [world slots][2 jobs][B][bmax][n] fp32
+ * (skei_rs_recv_floats), slot s written only by rank s, job 0 = x_fbp, job 1 = grad.
+ * q, r: this rank's m sketched rows [B][m][n_det] (device); idx, idx_stride as skei_fbp;
+ * peer_recv: HOST array of `world` (<= 8) device pointers to the ranks' receive buffers,
+ * valid on this GPU (this rank's own among them).  Errors: SKEI_ERR_SHAPE (B, m),
+ * SKEI_ERR_ARG (NULL, strides, m_total < m, world / rank out of range). */
+size_t skei_rs_recv_floats(const skei_plan *plan, int32_t B, int32_t world);
+skei_status skei_backproject_scatter(const skei_plan *plan, int32_t B, const float *q,
+                                     const float *r, const int32_t *idx, int32_t m,
+                                     int32_t idx_stride, int32_t m_total,
+                                     float *const *peer_recv, int32_t world, int32_t rank,
+                                     skei_stream stream);
+/* The receive side, after a cross-rank barrier (every rank's scatter has landed): this
+ * rank's band of x_fbp and grad, xfbp_band / grad_band [B][rows][n], as the world slots of
+ * recv (this rank's receive buffer) summed in slot (rank) order — fixed order, bitwise
+ * reproducible — and the band's ei partial sum_(band) (x2 - x_fbp)^2 into ei_band [B] (x2:
+ * whole images [B][n][n]; per-CTA partials summed in CTA order in fp64).  An all-reduce of
+ * the B ei partials (and the mc partials) completes the losses.  ws >=
+ * skei_workspace_bytes(plan, B, 1).  Errors: SKEI_ERR_SHAPE (B < 1), SKEI_ERR_ARG. */
+skei_status skei_band_reduce(const skei_plan *plan, int32_t B, const float *recv, int32_t world,
+                             int32_t rank, const float *x2, float *xfbp_band, float *grad_band,
+                             float *ei_band, void *ws, size_t ws_bytes, skei_stream stream);
+
 /* ------------------- next row: the Theorem-1 sketching deviation --
  * delta = ||A^T (S^T S - I) A||_2 (Theorem 1, proof L575-L583) for the
  * sqrt(n_full/m)-scaled row subsampling onto the sketched angles idx, by `iters` power
@@ -284,13 +316,15 @@ skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const f
 /* End-to-end variant from HOST buffers: copies host x1 [B][n][n], host y
  * [B][n_full][n_det], host g [B or 1] and host idx into the caller's device
  * buffers (d_x1, d_y, d_g, d_idx, same shapes), runs skei_pass, and copies
- * mc/ei back into host h_mc[B], h_ei[B].  With one sketch for the batch
- * (idx_stride 0) only the m sketched rows of y cross the link, into the head of d_y
- * as y_S [B][m][n_det] (the pass only reads y_S, Alg. 1 step 6): if h_ystage (host,
- * >= B*m*n_det floats, pinned) is given, the rows are gathered into it on the calling
- * thread and sent as one copy; else one strided copy per run of consecutive angle
- * indices.  h_ystage is rewritten at call time, so a previous call's copy from it must
- * have completed.  Per-image sketches copy all of y (h_ystage unused, may be NULL).
+ * mc/ei back into host h_mc[B], h_ei[B].  If h_ystage (host, >= B*m*n_det floats,
+ * pinned) is given, only the m sketched rows of each image's y cross the link (the
+ * pass only reads y_S, Alg. 1 step 6): image b's rows idx_b[0..m) (its own sketch when
+ * idx_stride = m) are gathered into it on the calling thread (up to 8 host threads for
+ * batches over 4 MB of rows) and sent as one copy into the head of d_y as y_S
+ * [B][m][n_det].  h_ystage is rewritten at call time, so a previous call's copy from it
+ * must have completed.  Without h_ystage (may be NULL) a shared sketch (idx_stride 0)
+ * uses one strided copy per run of consecutive angle indices and per-image sketches
+ * copy all of y.
  * Results are identical to skei_pass on device copies.  Host buffers should be
  * pinned for the copies to be asynchronous.  The caller synchronises `stream`
  * before reading h_mc / h_ei.  Errors: as skei_pass; SKEI_ERR_ARG if a host

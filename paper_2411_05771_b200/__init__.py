@@ -90,6 +90,10 @@ def lib():
             "skei_ramp_allgather": ([vp, i32, vp, vp, i32, i32, i32, vp, vp, vp, i32, vp], st),
             "skei_backproject_band": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp, vp,
                                        vp, vp, sz, vp], st),
+            "skei_rs_recv_floats": ([vp, i32, i32], sz),
+            "skei_backproject_scatter": ([vp, i32, vp, vp, vp, i32, i32, i32, vp, i32, i32, vp],
+                                         st),
+            "skei_band_reduce": ([vp, i32, vp, i32, i32, vp, vp, vp, vp, vp, sz, vp], st),
             "skei_radon_fwd": ([vp, vp, vp, i32, vp, i32, i32, vp, sz, vp], st),
             "skei_radon_adj": ([vp, vp, vp, i32, vp, i32, i32, ctypes.c_float, vp], st),
             "skei_ramp_filter": ([vp, vp, vp, i32, vp], st),
@@ -286,6 +290,43 @@ def backproject_band(plan: Plan, q: torch.Tensor, r: torch.Tensor, idx: torch.Te
                                        int(rows), _ptr(xf, name="xfbp"), _ptr(gr, name="grad"),
                                        _ptr(ei, name="ei"), _ptr(ws, torch.uint8, "ws"),
                                        ws.numel(), _stream(q)), "skei_backproject_band")
+    return xf, gr, ei
+
+
+def rs_recv_floats(plan: Plan, B: int, world: int) -> int:
+    """skei_rs_recv_floats: floats of one rank's receive buffer [world][2][B][bmax][n]."""
+    return int(lib().skei_rs_recv_floats(plan.handle, int(B), int(world)))
+
+
+def backproject_scatter(plan: Plan, q: torch.Tensor, r: torch.Tensor, idx: torch.Tensor,
+                        m_total: int, peer_recv: list, rank: int):
+    """skei_backproject_scatter: this rank's angle-shard partials of x_fbp and grad, every
+    output row stored by the kernel's epilogue into its band owner's receive buffer (device
+    pointers, ints; slot `rank`)."""
+    B, m = q.shape[0], idx.shape[-1]
+    n = len(peer_recv)
+    arr = (ctypes.c_void_p * n)(*[ctypes.c_void_p(int(x)) for x in peer_recv])
+    _check(lib().skei_backproject_scatter(plan.handle, B, _ptr(q, name="q"), _ptr(r, name="r"),
+                                          _ptr(idx, torch.int32, "idx"), m,
+                                          _idx_stride(idx, B, m), int(m_total), arr, n,
+                                          int(rank), _stream(q)), "skei_backproject_scatter")
+
+
+def band_reduce(plan: Plan, recv: torch.Tensor, world: int, rank: int, x2: torch.Tensor,
+                ws: torch.Tensor | None = None):
+    """skei_band_reduce: (x_fbp band, grad band, ei band partial) of `rank` from its receive
+    buffer (the world slots summed in rank order)."""
+    B, n = x2.shape[0], plan.n
+    q, rem = divmod(n, world)
+    rows = q + (1 if rank < rem else 0)
+    xf = torch.empty(B, rows, n, dtype=torch.float32, device=x2.device)
+    gr = torch.empty_like(xf)
+    ei = torch.empty(B, dtype=torch.float32, device=x2.device)
+    ws = plan.workspace(B, 1) if ws is None else ws
+    _check(lib().skei_band_reduce(plan.handle, B, _ptr(recv, name="recv"), int(world), int(rank),
+                                  _ptr(x2, name="x2"), _ptr(xf, name="xfbp"), _ptr(gr, name="grad"),
+                                  _ptr(ei, name="ei"), _ptr(ws, torch.uint8, "ws"), ws.numel(),
+                                  _stream(x2)), "skei_band_reduce")
     return xf, gr, ei
 
 

@@ -4,7 +4,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -426,6 +428,65 @@ skei_status skei_backproject_band(const skei_plan *plan, int32_t B, const float 
     return SKEI_OK;
 }
 
+namespace {
+// row band of `rank` when n rows are split over `world` ranks (dist.batch_range)
+void band_of(int n, int rank, int world, int *row0, int *rows) {
+    const int q = n / world, rem = n - q * world;
+    *row0 = rank * q + (rank < rem ? rank : rem);
+    *rows = q + (rank < rem ? 1 : 0);
+}
+}  // namespace
+
+size_t skei_rs_recv_floats(const skei_plan *plan, int32_t B, int32_t world) {
+    if (!plan || B < 1 || world < 1) return 0;
+    const size_t bmax = ((size_t)plan->n + world - 1) / world;
+    return (size_t)world * 2 * B * bmax * plan->n;
+}
+
+skei_status skei_backproject_scatter(const skei_plan *plan, int32_t B, const float *q,
+                                     const float *r, const int32_t *idx, int32_t m,
+                                     int32_t idx_stride, int32_t m_total,
+                                     float *const *peer_recv, int32_t world, int32_t rank,
+                                     skei_stream stream) {
+    skei_status st = check_idx_args(plan, B, idx, m, idx_stride);
+    if (st != SKEI_OK) return st;
+    if (!q || !r || !peer_recv || m_total < m) return SKEI_ERR_ARG;
+    if (world < 1 || world > kMaxRsPeers || rank < 0 || rank >= world || world > plan->n)
+        return SKEI_ERR_ARG;
+    AdjRs rs;
+    rs.world = world;
+    rs.bmax = (plan->n + world - 1) / world;
+    const size_t slot = (size_t)2 * B * rs.bmax * plan->n;
+    for (int o = 0; o < kMaxRsPeers; ++o) {
+        rs.peer[o] = o < world ? peer_recv[o] : nullptr;
+        if (o < world && !rs.peer[o]) return SKEI_ERR_ARG;
+        if (o < world) rs.peer[o] += (size_t)rank * slot;  // this rank's slot
+    }
+    DeviceGuard guard(plan->device);
+    AdjJob aj[2] = {{q, nullptr, (float)(M_PI / (2.0 * (double)m_total))}, {r, nullptr, 2.0f}};
+    SKEI_CUDA(launch_radon_adj(plan, aj, 2, B, idx, m, idx_stride, (cudaStream_t)stream, nullptr,
+                               0, -1, false, &rs));
+    return SKEI_OK;
+}
+
+skei_status skei_band_reduce(const skei_plan *plan, int32_t B, const float *recv, int32_t world,
+                             int32_t rank, const float *x2, float *xfbp_band, float *grad_band,
+                             float *ei_band, void *ws, size_t ws_bytes, skei_stream stream) {
+    if (!plan || !recv || !x2 || !xfbp_band || !grad_band || !ei_band || !ws) return SKEI_ERR_ARG;
+    if (B < 1) return SKEI_ERR_SHAPE;
+    if (world < 1 || world > kMaxRsPeers || rank < 0 || rank >= world || world > plan->n)
+        return SKEI_ERR_ARG;
+    if (ws_bytes < skei_workspace_bytes(plan, B, 1)) return SKEI_ERR_ARG;
+    int row0, rows;
+    band_of(plan->n, rank, world, &row0, &rows);
+    DeviceGuard guard(plan->device);
+    const WsLayout wl = ws_layout(plan, B, 1);
+    SKEI_CUDA(launch_band_reduce(recv, world, B, (plan->n + world - 1) / world, plan->n, row0,
+                                 rows, x2, xfbp_band, grad_band, ei_band, ws_f(ws, wl.eipart),
+                                 (cudaStream_t)stream));
+    return SKEI_OK;
+}
+
 skei_status skei_sketch_deviation(const skei_plan *plan, int32_t B, const int32_t *idx,
                                   int32_t m, int32_t idx_stride, int32_t iters, float *v,
                                   float *lambda, void *ws, size_t ws_bytes, skei_stream stream) {
@@ -733,23 +794,39 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
     const size_t nn = (size_t)plan->n * plan->n, ny = (size_t)plan->n_full * plan->n_det;
     SKEI_CUDA(cudaMemcpyAsync(d_x1, h_x1, sizeof(float) * B * nn, cudaMemcpyHostToDevice, s));
     const int n_det = plan->n_det;
-    // With one sketch for the batch only the m sketched rows of y cross the link: each run
-    // of consecutive angle indices is one strided copy of B row blocks, into d_y as y_S
-    // [B][m][n_det] (the pass then reads y_S row k for angle idx[k]).  Per-image sketches
-    // copy the whole of y.
-    const bool y_sk = idx_stride == 0;
-    if (y_sk && h_ystage) {  // host gather of the sketched rows, then one copy
-        for (int b = 0; b < B; ++b)
-            for (int k = 0; k < m;) {
-                int e = k + 1;
-                while (e < m && h_idx[e] == h_idx[e - 1] + 1) ++e;
-                std::memcpy(h_ystage + ((size_t)b * m + k) * n_det,
-                            h_y + (size_t)b * ny + (size_t)h_idx[k] * n_det,
-                            sizeof(float) * (e - k) * n_det);
-                k = e;
+    // Only the m sketched rows of each image's y cross the link, into d_y as y_S
+    // [B][m][n_det] (the pass then reads y_S row k of image b for angle idx_b[k]).  With a
+    // staging buffer each image's rows (its own sketch when idx_stride = m) are gathered
+    // into it and sent as one copy; without one, a shared sketch uses one strided copy of B
+    // row blocks per run of consecutive angle indices and per-image sketches copy all of y.
+    const bool y_sk = idx_stride == 0 || h_ystage;
+    if (h_ystage) {
+        auto gather = [=](int b0, int b1) {
+            for (int b = b0; b < b1; ++b) {
+                const int32_t *ib = h_idx + (size_t)b * idx_stride;
+                for (int k = 0; k < m;) {
+                    int e = k + 1;
+                    while (e < m && ib[e] == ib[e - 1] + 1) ++e;
+                    std::memcpy(h_ystage + ((size_t)b * m + k) * n_det,
+                                h_y + (size_t)b * ny + (size_t)ib[k] * n_det,
+                                sizeof(float) * (e - k) * n_det);
+                    k = e;
+                }
             }
-        SKEI_CUDA(cudaMemcpyAsync(d_y, h_ystage, sizeof(float) * B * m * n_det,
-                                  cudaMemcpyHostToDevice, s));
+        };
+        // large batches (cfg4: 33 MB of rows) are gathered by a few host threads
+        const size_t bytes = sizeof(float) * (size_t)B * m * n_det;
+        const int nt = (int)std::min<size_t>({(size_t)B, (size_t)8, bytes / (4u << 20) + 1});
+        if (nt <= 1) {
+            gather(0, B);
+        } else {
+            std::vector<std::thread> th;
+            for (int t = 1; t < nt; ++t)
+                th.emplace_back(gather, (int)((long)B * t / nt), (int)((long)B * (t + 1) / nt));
+            gather(0, B / nt);
+            for (auto &t : th) t.join();
+        }
+        SKEI_CUDA(cudaMemcpyAsync(d_y, h_ystage, bytes, cudaMemcpyHostToDevice, s));
     } else if (y_sk) {
         for (int k = 0; k < m;) {
             int e = k + 1;

@@ -158,6 +158,16 @@ struct AdjEi {
     float *out;       // ei [B]
 };
 size_t adj_ei_part_floats(const skei_plan *plan, int B);
+// reduce-scatter epilogue: output row r of job j, image b is stored
+// (P2P over NVLink / symmetric memory) into the receive buffer of the rank o that owns row r
+// (bands as dist.batch_range(n, o, world): start(o) = o q + min(o, n mod world), q = n /
+// world), at peer[o] + ((j B + b) bmax + r - start(o)) n + c; peer[o] already points at this
+// rank's slot of rank o's buffer [world][2][B][bmax][n].  world 0: off.
+constexpr int kMaxRsPeers = 8;
+struct AdjRs {
+    float *peer[kMaxRsPeers];
+    int world = 0, bmax = 0;
+};
 // row0, rows: backproject only output rows [row0, row0 + rows) into [B][rows][n] outputs
 // (rows < 0: whole images)
 // fused: the two jobs are the slots of each image's group (job-fused pass): both jobs' pi
@@ -165,7 +175,15 @@ size_t adj_ei_part_floats(const skei_plan *plan, int B);
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
                              const AdjEi *ei = nullptr, int row0 = 0, int rows = -1,
-                             bool fused = false);
+                             bool fused = false, const AdjRs *rs = nullptr);
+// the receive side of the reduce-scatter: this rank's band [B][rows][n] of both jobs, the
+// world slots of recv [world][2][B][bmax][n] summed in slot (rank) order, and the band's ei
+// partial sum (x2 - x_fbp)^2 (x2 whole images [B][n][n], rows from row0) into ei [B];
+// part: >= B * band_reduce_part_floats(n, rows) floats of scratch
+size_t band_reduce_part_floats(int n, int rows);
+cudaError_t launch_band_reduce(const float *recv, int world, int B, int bmax, int n, int row0,
+                               int rows, const float *x2, float *xfbp, float *grad, float *ei,
+                               float *part, cudaStream_t s);
 
 void fft_plan(int P, int *npass, int *radix, int *ns, int *twoff, int *twtotal);
 // Theorem-1 deviation helpers (deviation.cu): part = [B][kNormChunks] fp64 chunk partials

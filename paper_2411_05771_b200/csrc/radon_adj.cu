@@ -55,7 +55,24 @@ struct AdjArgs {
     float *ei_part;
     unsigned *ei_ctr;
     float *ei_out;
+    AdjRs rs;  // reduce-scatter epilogue (rs.world > 0): outputs go to the row owners' slots
 };
+
+// where output (job jx, image img, row r, column c) is stored: the job's [B][row1 - row0][n]
+// output, or with the reduce-scatter epilogue the slot of r's band owner (P2P)
+__device__ __forceinline__ float *out_at(const AdjArgs &a, float *x, int jx, int img, int r,
+                                         int c, long &ox) {
+    const int n = a.g.n;
+    if (a.rs.world == 0) {
+        ox = (long)img * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
+        return x;
+    }
+    const int q = n / a.rs.world, rem = n - q * a.rs.world;
+    const int o = r < rem * (q + 1) ? r / (q + 1) : rem + (r - rem * (q + 1)) / q;
+    const int start = o * q + min(o, rem);
+    ox = ((long)(jx * a.B + img) * a.rs.bmax + (r - start)) * n + c;
+    return a.rs.peer[o];
+}
 
 template <int BB>
 struct Vec;
@@ -309,17 +326,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_radon_adj(AdjArgs a) {
                 const int img = FUSED ? b0 : b0 + b;
                 const float sc = jo.scale;
                 const long o = (long)img * nn + (long)r * n + c;  // in a whole image
-                const long ox = (long)img * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
+                long ox;
+                float *const dst = out_at(a, jo.x, FUSED ? b : jj, img, r, c, ox);
                 float v0 = sc * acc[jj][p][0][b], v1 = sc * acc[jj][p][1][b];
                 if (jo.base) {  // x = base + scale A^T p
                     if (c < n) v0 += __ldg(jo.base + ox);
                     if (c + 1 < n) v1 += __ldg(jo.base + ox + 1);
                 }
                 if (c + 1 < n && ((ox & 1) == 0)) {
-                    *reinterpret_cast<float2 *>(jo.x + ox) = make_float2(v0, v1);
+                    *reinterpret_cast<float2 *>(dst + ox) = make_float2(v0, v1);
                 } else {
-                    if (c < n) jo.x[ox] = v0;
-                    if (c + 1 < n) jo.x[ox + 1] = v1;
+                    if (c < n) dst[ox] = v0;
+                    if (c + 1 < n) dst[ox + 1] = v1;
                 }
                 if (jj == 0 && (!FUSED || b == 0) && a.ei_x2) {
                     if (c < n) {
@@ -620,7 +638,8 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
                 const int img = FUSED ? b0 : b0 + b;
                 const float sc = jo.scale;
                 const long o = (long)img * nn + (long)r * n + c;
-                const long ox = (long)img * (a.row1 - a.row0) * n + (long)(r - a.row0) * n + c;
+                long ox;
+                float *const dst = out_at(a, jo.x, FUSED ? b : jj, img, r, c, ox);
                 float v[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) v[k] = sc * acc[jj][k][b];
@@ -630,11 +649,11 @@ __global__ void __launch_bounds__(kThreads, FUSED ? SKEI_ADJQ_MINB_FUSED : SKEI_
                         if (c + k < n) v[k] += __ldg(jo.base + ox + k);
                 }
                 if (c + 3 < n && ((ox & 3) == 0)) {
-                    *reinterpret_cast<float4 *>(jo.x + ox) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4 *>(dst + ox) = make_float4(v[0], v[1], v[2], v[3]);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        if (c + k < n) jo.x[ox + k] = v[k];
+                        if (c + k < n) dst[ox + k] = v[k];
                 }
                 if (jj == 0 && (!FUSED || b == 0) && a.ei_x2) {
 #pragma unroll
@@ -742,9 +761,15 @@ size_t adj_ei_part_floats(const skei_plan *plan, int B) {
 
 cudaError_t launch_radon_adj(const skei_plan *plan, const AdjJob *jobs, int njobs, int B,
                              const int32_t *idx, int m, int idx_stride, cudaStream_t s,
-                             const AdjEi *ei, int row0, int rows, bool fused) {
+                             const AdjEi *ei, int row0, int rows, bool fused,
+                             const AdjRs *rs) {
     if (fused && (njobs != 2 || !jobs[0].pi)) return cudaErrorInvalidValue;
+    // the reduce-scatter epilogue: whole images, no base addend, no fused ei
+    if (rs && (rs->world < 1 || rs->world > kMaxRsPeers || row0 > 0 || rows >= 0 || ei ||
+               jobs[0].base || (njobs > 1 && jobs[1].base)))
+        return cudaErrorInvalidValue;
     AdjArgs a;
+    if (rs) a.rs = *rs;
     a.job[0] = jobs[0];
     a.job[1] = njobs > 1 ? jobs[1] : jobs[0];
     a.idx = idx;

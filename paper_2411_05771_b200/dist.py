@@ -33,7 +33,8 @@ import torch.distributed as dist
 
 __all__ = ["batch_range", "angle_shard", "CudaOps", "angle_split_pass", "batch_split_images",
            "angle_split_pass_allgather", "shard_phase", "band_phase", "angle_split_pass_p2p",
-           "P2PBuffers", "simulate_p2p_split"]
+           "P2PBuffers", "simulate_p2p_split", "RSBuffers", "rs_slot_offset",
+           "angle_split_pass_rs", "simulate_rs_split"]
 
 
 def batch_range(B: int, rank: int, world: int) -> range:
@@ -102,6 +103,14 @@ class CudaOps:
     def ramp_allgather(self, p, r, row0, m_total, peer_q, peer_r):
         import paper_2411_05771_b200 as sk
         return sk.ramp_allgather(self.plan, p, r, row0, m_total, peer_q, peer_r)
+
+    def backproject_scatter(self, q, r, idx, m_total, peer_recv, rank):
+        import paper_2411_05771_b200 as sk
+        return sk.backproject_scatter(self.plan, q, r, idx, m_total, peer_recv, rank)
+
+    def band_reduce(self, recv, world, rank, x2):
+        import paper_2411_05771_b200 as sk
+        return sk.band_reduce(self.plan, recv, world, rank, x2)
 
 
 def angle_split_pass(ops, x1, y, g, idx, group=None):
@@ -305,3 +314,112 @@ def simulate_p2p_split(ops, x1, y, g, idx, world: int):
     bands = [band_phase(ops, bufs[rk][0], bufs[rk][1], idx, x2, rk, world) for rk in range(world)]
     return {"x2": x2, "bands": bands, "mc": mc, "bufs": bufs}
 
+
+
+# ---------------------------------------------------------------------------------------
+# The split's other communication-reduced form: the backprojection's
+# reduce-scatter fused into the backprojector.  Every rank projects, filters and backprojects
+# only its angle shard; the adjoint kernel's epilogue stores each output row of the partial
+# x_fbp and grad straight into the receive buffer of the rank owning that row's band (P2P
+# stores into symmetric memory, slot = the sending rank), so the exchange — (G-1)/G x 2 B n^2
+# floats per GPU, half the all-reduce's — overlaps the backprojection tile by tile.  After a
+# device barrier each rank sums its G slots in rank order (skei_band_reduce: a fixed order,
+# bitwise reproducible) into its bands of x_fbp and grad plus the band's ei partial; one
+# all-reduce of 2 B scalars (mc, ei) completes the losses.  Outputs are row-sharded like the
+# all-gather form's; the rows are batch_range(n, rank, G).
+
+def rs_slot_offset(B: int, n: int, world: int, job: int, b: int, row: int, col: int):
+    """(owner rank, float offset within the owner's receive buffer slot) of output element
+    (job, image b, row, col) — the layout skei_backproject_scatter stores into (host mirror
+    of radon_adj.cu out_at, used by the CPU layout test)."""
+    q, rem = divmod(n, world)
+    o = row // (q + 1) if row < rem * (q + 1) else rem + (row - rem * (q + 1)) // q
+    start = batch_range(n, o, world).start
+    bmax = -(-n // world)
+    return o, ((job * B + b) * bmax + row - start) * n + col
+
+
+class RSBuffers:
+    """One receive buffer [world][2][B][bmax][n] per rank plus the peers' pointers: torch
+    symmetric memory over the group (world > 1), or a plain local tensor (world 1)."""
+
+    def __init__(self, B, n, device, group=None):
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.world = world
+        bmax = -(-n // world)
+        shape = (world, 2, B, bmax, n)
+        if world > 1:
+            import torch.distributed._symmetric_memory as symm
+            grp = group if group is not None else dist.group.WORLD
+            if hasattr(symm, "enable_symm_mem_for_group"):
+                symm.enable_symm_mem_for_group(grp.group_name)
+            self.buf = symm.empty(shape, dtype=torch.float32, device=device)
+            self.handle = symm.rendezvous(self.buf, grp.group_name)
+            self.peers = [int(p) for p in self.handle.buffer_ptrs]
+        else:
+            self.buf = torch.empty(shape, dtype=torch.float32, device=device)
+            self.handle = None
+            self.peers = [self.buf.data_ptr()]
+
+    def barrier(self, channel: int = 0):
+        if self.handle is not None:
+            self.handle.barrier(channel=channel)
+
+
+def angle_split_pass_rs(ops, x1, y, g, idx, group=None, bufs: RSBuffers | None = None):
+    """One pass with the sketch `idx` split over the ranks of `group`, the backprojection's
+    reduce-scatter fused into the backprojector (comment above); outputs as
+    angle_split_pass_allgather (row bands of x_fbp and grad, complete mc and ei)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    m = len(idx)
+    sub = angle_shard(idx, rank, world)
+    x2 = ops.rotate(x1, g)
+    p1 = ops.forward(x1, sub)
+    p2 = ops.forward(x2, sub)
+    mc_part, r = ops.residual(p1, y, sub)
+    q = ops.ramp(p2)
+    B, N = x1.shape[0], x1.shape[-1]
+    if bufs is None:
+        bufs = RSBuffers(B, N, x1.device, group)
+    else:
+        # reused buffers: no rank may store into a peer's slots while that peer still sums
+        # them for the previous pass (write-after-read across ranks)
+        bufs.barrier(channel=1)
+    ops.backproject_scatter(q, r, sub, m, bufs.peers, rank)
+    bufs.barrier()
+    xf, gr, ei = ops.band_reduce(bufs.buf, world, rank, x2)
+    scal = torch.cat([mc_part.to(ei.dtype), ei])
+    if world > 1:
+        dist.all_reduce(scal, op=dist.ReduceOp.SUM, group=group)
+    return {"x2": x2, "xfbp": xf, "grad": gr, "rows": batch_range(N, rank, world),
+            "mc": scal[:B], "ei": scal[B:], "idx": sub,
+            "rs_bytes": 2 * B * N * N * 4 * (world - 1) // max(world, 1)}
+
+
+def simulate_rs_split(ops, x1, y, g, idx, world: int):
+    """The reduce-scatter split's data path on ONE GPU: `world` virtual ranks with their own
+    receive buffers; every virtual rank's backprojector stores its partial rows into all of
+    them (the same kernel and pointer lists as across GPUs), then each virtual rank sums its
+    slots.  Returns the per-rank bands (x_fbp, grad, ei partial) and the summed mc (test
+    helper)."""
+    m = len(idx)
+    x2 = ops.rotate(x1, g)
+    B, N = x1.shape[0], x1.shape[-1]
+    bmax = -(-N // world)
+    bufs = [torch.full((world, 2, B, bmax, N), float("nan"), dtype=torch.float32,
+                       device=x1.device) for _ in range(world)]
+    peers = [b.data_ptr() for b in bufs]
+    mc = torch.zeros(B, dtype=torch.float32, device=x1.device)
+    for rk in range(world):
+        sub = angle_shard(idx, rk, world)
+        p1 = ops.forward(x1, sub)
+        p2 = ops.forward(x2, sub)
+        mc_part, r = ops.residual(p1, y, sub)
+        ops.backproject_scatter(ops.ramp(p2), r, sub, m, peers, rk)
+        mc += mc_part
+    bands = []
+    for rk in range(world):
+        xf, gr, ei = ops.band_reduce(bufs[rk], world, rk, x2)
+        bands.append({"rows": batch_range(N, rk, world), "xfbp": xf, "grad": gr, "ei": ei})
+    return {"x2": x2, "bands": bands, "mc": mc, "bufs": bufs}

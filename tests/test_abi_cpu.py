@@ -26,7 +26,7 @@ def _declared_functions():
 
 def test_library_exports_every_declared_symbol():
     names = _declared_functions()
-    assert len(names) == 27
+    assert len(names) == 30
     L = ctypes.CDLL(sk.lib_path)
     for name in names:
         assert hasattr(L, name), name
@@ -44,6 +44,9 @@ def test_host_validation_without_device():
     assert L.skei_radon_fwd(None, None, None, 1, None, 1, 0, None, 0, None) == 3
     assert L.skei_ramp_filter(None, None, None, 1, None) == 3
     assert L.skei_rotate_adjoint(None, None, None, 1, None, 0, None) == 3
+    assert L.skei_backproject_scatter(None, 1, None, None, None, 1, 0, 1, None, 2, 0, None) == 3
+    assert L.skei_band_reduce(None, 1, None, 2, 0, None, None, None, None, None, 0, None) == 3
+    assert L.skei_rs_recv_floats(None, 1, 2) == 0
     assert L.skei_plan_create(None, 0, None) == 3
     g = sk._Geom(64, 91, 32, 100)  # fft_len not a power of two -> config error
     h = ctypes.c_void_p()

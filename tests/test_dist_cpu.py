@@ -222,3 +222,45 @@ def test_allgather_volume():
     # cfg5: 2 B m n_det fp32 = 2,967,552 bytes exchanged vs 8,388,612 all-reduced
     assert skdist.allgather_bytes(1, 256, 1449) == 2967552
 
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_rs_layout_reduces_to_full_pass(world):
+    """SURVEY §8(f) #2 (b) host logic: each virtual rank's oracle partials (its angle shard,
+    the full sketch's density scale) placed by rs_slot_offset — the layout the backprojector's
+    reduce-scatter epilogue stores into — and each owner's slots summed in rank order give
+    the bands of the full-sketch pass's x_fbp and grad; every band row is stored exactly once
+    per slot, and the bands tile the image (rows from batch_range)."""
+    cfg, x1, y, g, idx = _inputs()
+    ops = make_ops(cfg)
+    B, N, m = cfg.B, cfg.N, len(idx)
+    bmax = -(-N // world)
+    recv = [np.full((world, 2 * B * bmax * N), np.nan) for _ in range(world)]
+    x2 = torch.stack([ops.rotate(x1[b], g) for b in range(B)])
+    for rk in range(world):
+        sub = skdist.angle_shard(idx, rk, world)
+        p1 = torch.stack([ops.forward(x1[b], sub) for b in range(B)])
+        p2 = torch.stack([ops.forward(x2[b], sub) for b in range(B)])
+        _, r = ops.residual(p1, y, sub)
+        parts = [torch.stack([ops.fbp(p2[b], sub, m) for b in range(B)]).numpy(),
+                 torch.stack([ops.adjoint(r[b], sub, 2.0) for b in range(B)]).numpy()]
+        for j in range(2):
+            for b in range(B):
+                for row in range(N):
+                    o, off = skdist.rs_slot_offset(B, N, world, j, b, row, 0)
+                    assert np.isnan(recv[o][rk, off:off + N]).all(), "stored twice"
+                    recv[o][rk, off:off + N] = parts[j][b, row]
+    rows_seen = []
+    for o in range(world):
+        band = skdist.batch_range(N, o, world)
+        rows_seen += list(band)
+        slots = recv[o].reshape(world, 2, B, bmax, N)[:, :, :, :len(band)]
+        assert not np.isnan(slots).any()
+        acc = np.zeros_like(slots[0])
+        for s in range(world):
+            acc = acc + slots[s]
+        for b in range(B):
+            ref = oracle.sketched_pass(x1[b].numpy(), y[b].numpy(), g, idx, cfg.n_full)
+            np.testing.assert_allclose(acc[0, b], ref["xfbp"][band.start:band.stop], rtol=0, atol=1e-11)
+            np.testing.assert_allclose(acc[1, b], ref["grad"][band.start:band.stop], rtol=0, atol=1e-11)
+    assert rows_seen == list(range(N))

@@ -189,3 +189,67 @@ def test_p2p_split_single_rank_equals_pass():
     full = sk.sketched_pass(plan, x1, y, g, idx)
     for k in ("x2", "xfbp", "grad", "mc", "ei"):
         _close(out[k], full[k], k)
+
+
+@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 3), ("cfg5", 4), ("cfg5", 8)])
+def test_rs_fused_split_bands_tile_full_pass(name, world):
+    """the backprojection's reduce-scatter fused into the backprojector
+    (every output row stored into its band owner's slot), simulated on one GPU with `world`
+    virtual ranks and real pointer lists.  The bands tile x_fbp and grad of the single-GPU
+    pass and of the oracle (partition identity of PAPER.md L70 / L92); each band equals its
+    slots summed in rank order bit for bit; the slot rows beyond a band are never read."""
+    cfg = synth.CONFIGS[name]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    out = skdist.simulate_rs_split(skdist.CudaOps(plan), x1, y, g, idx[0], world)
+    bands = out["bands"]
+    for rk, bd in enumerate(bands):
+        nrows = len(bd["rows"])
+        assert bd["rows"] == skdist.batch_range(cfg.N, rk, world)
+        slots = out["bufs"][rk][:, :, :, :nrows]
+        assert not torch.isnan(slots).any(), "a slot row of the band was not stored"
+        acc = torch.zeros_like(slots[0])
+        for s in range(world):  # slot (rank) order, as the reduce kernel
+            acc = acc + slots[s]
+        assert torch.equal(bd["xfbp"], acc[0]) and torch.equal(bd["grad"], acc[1])
+    _close(torch.cat([bd["xfbp"] for bd in bands], dim=1), full["xfbp"], "xfbp bands")
+    _close(torch.cat([bd["grad"] for bd in bands], dim=1), full["grad"], "grad bands")
+    _close(out["mc"], full["mc"], "mc")
+    _close(sum(bd["ei"] for bd in bands), full["ei"], "ei")
+    _check_split_vs_oracle(cfg, x1n, yn, bands, out["mc"], sum(bd["ei"] for bd in bands))
+    # deterministic: a second run stores and sums the same bits
+    again = skdist.simulate_rs_split(skdist.CudaOps(plan), x1, y, g, idx[0], world)
+    for a, b in zip(bands, again["bands"]):
+        assert torch.equal(a["xfbp"], b["xfbp"]) and torch.equal(a["grad"], b["grad"])
+        assert torch.equal(a["ei"], b["ei"])
+
+
+def test_rs_split_single_rank_equals_pass():
+    cfg = synth.CONFIGS["cfg1"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    x1n, yn = synth.make_workload(cfg, seed=0)
+    x1 = torch.from_numpy(x1n).cuda()
+    y = torch.from_numpy(yn).cuda()
+    g, idx = sk.draw_device(0, 0, 0, 1, True, cfg.n_full, cfg.m)
+    out = skdist.angle_split_pass_rs(skdist.CudaOps(plan), x1, y, g, idx[0])
+    full = sk.sketched_pass(plan, x1, y, g, idx)
+    for k in ("x2", "xfbp", "grad", "mc", "ei"):
+        _close(out[k], full[k], k)
+
+
+def test_rs_scatter_rejects_bad_arguments():
+    cfg = synth.CONFIGS["cfg1"]
+    plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
+    q = torch.zeros(1, 4, cfg.n_det, device="cuda")
+    idx = torch.arange(4, dtype=torch.int32, device="cuda")
+    buf = torch.zeros(sk.rs_recv_floats(plan, 1, 2), device="cuda")
+    with pytest.raises(sk.SkeiError):  # rank outside the world
+        sk.backproject_scatter(plan, q, q, idx, 4, [buf.data_ptr()] * 2, 2)
+    with pytest.raises(sk.SkeiError):  # more than 8 peers
+        sk.backproject_scatter(plan, q, q, idx, 4, [buf.data_ptr()] * 9, 0)
+    with pytest.raises(sk.SkeiError):  # m_total < m
+        sk.backproject_scatter(plan, q, q, idx, 3, [buf.data_ptr()] * 2, 0)

@@ -410,10 +410,14 @@ def test_gpu_adjoint_identity():
 @pytest.mark.parametrize("name,shared,mode", [("cfg1", True, sk.MODE_UNIFORM),
                                               ("cfg2", True, sk.MODE_UNIFORM),
                                               ("cfg2", True, sk.MODE_INTERLEAVED),
-                                              ("cfg2", False, sk.MODE_UNIFORM)])
+                                              ("cfg2", False, sk.MODE_UNIFORM),
+                                              ("cfg2", False, sk.MODE_INTERLEAVED),
+                                              ("cfg4", False, sk.MODE_UNIFORM)])
 def test_pass_host_matches_device_pass(name, shared, mode, stage):
-    """skei_pass_host (a shared sketch copies only y's sketched rows, as strided copies of
-    runs of consecutive angles) gives exactly skei_pass's results on device copies."""
+    """skei_pass_host (only y's sketched rows cross the link: gathered per image into the
+    staging buffer — each image's own rows for per-image sketches, several host threads at
+    cfg4 — or, for a shared sketch without one, strided copies of runs of consecutive
+    angles) gives exactly skei_pass's results on device copies."""
     cfg = synth.CONFIGS[name]
     plan = sk.Plan.get(cfg.N, cfg.n_det, cfg.n_full, cfg.fft_len)
     x1, y = synth.make_workload(cfg)

@@ -10,7 +10,7 @@ python bench.py --mode interleaved --no-cpu-baseline > gpurun_out/sweep/cfg3_il.
 for p in ei-grad rei deviation; do
   python bench.py --path $p --no-cpu-baseline > gpurun_out/sweep/$p.json 2> gpurun_out/sweep/$p.err
 done
-for s in angle angle-ag angle-p2p; do
+for s in angle angle-ag angle-p2p angle-rs; do
   python bench.py --config cfg5 --split $s --no-cpu-baseline --no-e2e > gpurun_out/sweep/cfg5_$s.json 2> gpurun_out/sweep/cfg5_$s.err
 done
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/sweep/reference.json 2> gpurun_out/sweep/reference.err
