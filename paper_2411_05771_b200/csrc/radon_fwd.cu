@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
 
 #ifdef SKEI_FWD_STATS
     long long st_wait = 0, st_epi = 0, st_pro = 0, st_active = 0, st_lanes = 0;
+    long long st_tc[kMaxT] = {}, st_tn[kMaxT] = {};  // per task slot: cycles, active blocks
     const long long st_t0 = clock64();
 #endif
     int gbase = 0;  // stream index of the current unit's first block
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 if (t + 1 < kMaxT) tdn = s_task[warp + kWarps * (t + 1)];
                 if (td.y > ent.w || td.y + kChunk - 1 < ent.z) continue;  // chunk misses the block
 #ifdef SKEI_FWD_STATS
+                const long long tt0 = clock64();
                 ++st_active;
                 st_lanes += max(0, min(td.y + kChunk - 1, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
 #endif
@@ -822,6 +824,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
 #else
                 run_lines(std::true_type{});
 #endif
+#ifdef SKEI_FWD_STATS
+#pragma unroll
+                for (int tt = 0; tt < kMaxT; ++tt)
+                    if (tt == t) {
+                        st_tc[tt] += clock64() - tt0;
+                        ++st_tn[tt];
+                    }
+#endif
                 if constexpr (kUnrollT) {
 #pragma unroll
                     for (int b = 0; b < BB; ++b) {
@@ -853,6 +863,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
         }
 
 #ifdef SKEI_FWD_STATS
+        if (lane == 0 && (blockIdx.x % SKEI_FWD_STATS_EVERY) == 0) {
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t) {
+                const int4 td = s_task[warp + kWarps * t];
+                if (td.x < 0) continue;
+                printf("FWDTASK cta %d warp %d slot %d ab1e4 %d c0 %d cost %d blocks %lld cycles %lld cls %d\n",
+                       blockIdx.x, warp, t, (int)(sAngT[td.x][0].x * 10000.f), td.y,
+                       s_cost[td.x * a.chunks + td.y / kChunk], st_tn[t], st_tc[t], d.cls);
+                st_tn[t] = st_tc[t] = 0;
+            }
+        }
         const long long te0 = clock64();
 #endif
         // ---- 4. unit epilogue.  A whole unit is complete in this CTA's registers: each lane

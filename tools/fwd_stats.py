@@ -25,6 +25,8 @@ def main():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1",
                           "--warmup", "3", "--no-cpu-baseline", "--no-e2e"],
                          env=dict(os.environ, SKEI_LIB=lib), capture_output=True, text=True).stdout
+    if os.environ.get("STATS_RAW"):  # keep the raw records (FWDSTAT per warp, FWDTASK per task)
+        open(os.environ["STATS_RAW"], "w").write(out)
     rows = [list(map(int, re.findall(r"-?\d+", l))) for l in out.splitlines() if "FWDSTAT" in l]
     # cta warp units G wait pro epi total
     print("launch-CTA-warp records", len(rows), "median total cycles", st.median(r[7] for r in rows))
