@@ -122,6 +122,19 @@ constexpr int kMaxBand = 64;     // band angles of the source class considered f
 #ifndef SKEI_FWD_BAND
 #define SKEI_FWD_BAND 1  // flexible class band near the diagonals (A/B knob)
 #endif
+// Floating tasks (A/B knob, off): the unit's SKEI_FWD_FLOAT costliest tasks are not dealt to a
+// warp; a warp done with its own tasks of a staged block takes them from the block's queue
+// and adds their block sums, in block order, to sums kept in shared memory (bitwise the
+// same results; parity suite green with 10).  Measured at cfg3 (round 2, session 5): the
+// warps' mbarrier wait fell from 13% to 3% of their time, but every (task, block) pair got
+// 16-20% slower and the kernel went from 264.8 to 269.5 us (6 floating tasks: 278.6): with
+// all 16 warps busy the SM's shared-memory pipe / issue slots are the limit, i.e. the "wait"
+// of the static deal is time in which the other warps run faster, not idle capacity.
+#ifndef SKEI_FWD_FLOAT
+#define SKEI_FWD_FLOAT 0
+#endif
+constexpr int kMaxFloat = SKEI_FWD_FLOAT < kWarps ? SKEI_FWD_FLOAT : kWarps;
+constexpr int kFloatBytes = 32 * 2 * 4 * (int)sizeof(float);  // a floating task's sums (BB = 4)
 constexpr int kCand = 5;    // candidate pixels of a bin pair per line
 constexpr int kPadL = 5;    // zero pixel columns left of the line data (candidates from -5)
 constexpr int kPadR = 8;    // ... and right of it (candidates reach n + 4; a column block
@@ -137,6 +150,7 @@ struct FwdArgs {
     // x2 of one image share its sketch, so they share the projector's geometry); job[0].xr /
     // xc hold the fused packed layout, slot b's projections go to job[b].p, MC on slot 0
     int fused;
+    int nfloat;  // floating tasks per unit (<= kMaxFloat; 0: every task is pinned to a warp)
     int K;       // angles per unit: K * chunks <= kWarps * kMaxT tasks
     int chunks;  // ceil(n_det / 32)
     int nblk;    // packed blocks per image group (ceil(n / R))
@@ -289,6 +303,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
     __shared__ bool s_last;
     __shared__ int4 s_task[kWarps * kMaxT];  // per task: angle slot, chunk bin, chunk Pj split
     __shared__ int s_cost[kWarps * kMaxT];   // per task: blocks its chunk touches
+    // floating tasks (the unit's costliest): any warp that has finished its own tasks of a
+    // staged block takes them from the block's queue; their running sums live in shared memory
+    __shared__ int4 s_float[kMaxFloat > 0 ? kMaxFloat : 1];
+    __shared__ int s_fseq[kMaxFloat > 0 ? kMaxFloat : 1];  // next block whose sum may be added
+    __shared__ int s_fq[3];                                // per buffer: grabs so far (unit)
+    __shared__ int s_nfl;
     __shared__ int s_defer[2], s_dnpc[2];  // split units this CTA finishes after its stream
     __shared__ int s_dpiece[2][kMaxPieces];  // ... their piece slots in CTA order
 
@@ -298,6 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int stage_f = (n + kPadL + kPadR) * kColF;
     int4 *btab = reinterpret_cast<int4 *>(smem + a.nbuf * stage_f);  // [K][nb] block table
+    // [nfloat][32 lanes][2 BB] sums of the floating tasks, behind the block table
+    float *facc = reinterpret_cast<float *>(btab + (size_t)a.K * a.nblk);
+    constexpr bool kFloat = kMaxFloat > 0 && BB == 4 && !FUSED;
+    const int nfloat = kFloat ? a.nfloat : 0;
     const long part_f = (long)K * n_det * BB;
     SKEI_DCHECK(part_f <= (long)kWarps * kMaxTaskBB * kChunk && ncl <= kMaxPieces && K <= kKMax &&
                     nq <= kMaxQ,
@@ -503,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
 #ifdef SKEI_FWD_STATS
     long long st_wait = 0, st_epi = 0, st_pro = 0, st_active = 0, st_lanes = 0;
     long long st_tc[kMaxT] = {}, st_tn[kMaxT] = {};  // per task slot: cycles, active blocks
+    long long st_fl = 0;  // floating (task, block) pairs this warp ran
     const long long st_t0 = clock64();
 #endif
     int gbase = 0;  // stream index of the current unit's first block
@@ -631,6 +656,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
         __syncthreads();  // block table and task costs complete
         for (int tau = threadIdx.x; tau < kWarps * kMaxT; tau += kThreads)
             s_task[tau] = make_int4(-1, 0, 0, 0);
+        if (threadIdx.x < 3) s_fq[threadIdx.x] = 0;
+        if (threadIdx.x == 3) s_nfl = 0;
+        if (threadIdx.x >= 32 && threadIdx.x < 32 + kMaxFloat) s_fseq[threadIdx.x - 32] = -1;
         __syncthreads();
         for (int tau = threadIdx.x; tau < ntask; tau += kThreads) {
             const int cst = s_cost[tau];
@@ -640,8 +668,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 const int co = s_cost[o];
                 r += (co > cst) || (co == cst && o < tau);
             }
-            const int round = r / kWarps, wi = r - round * kWarps;
-            const int w = (round & 1) ? kWarps - 1 - wi : wi;
             int4 td;
             td.x = tau / a.chunks;
             td.y = (tau - td.x * a.chunks) * kChunk;
@@ -649,9 +675,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
             const double fJ = floor(J);
             td.z = (int)fJ;
             td.w = __float_as_int((float)(J - fJ));
+            if (r < nfloat) {  // the costliest tasks float (they touch the most blocks)
+                s_float[r] = td;
+                atomicMax(&s_nfl, r + 1);
+                continue;
+            }
+            r -= nfloat;
+            const int round = r / kWarps, wi = r - round * kWarps;
+            const int w = (round & 1) ? kWarps - 1 - wi : wi;
             s_task[w + kWarps * round] = td;
         }
         __syncthreads();  // block table and task table complete
+        const int nfl = kFloat ? s_nfl : 0;
 #ifdef SKEI_FWD_STATS
         st_pro += clock64() - tp0;
 #endif
@@ -674,23 +709,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
 #ifdef SKEI_FWD_STATS
             st_wait += clock64() - tw0;
 #endif
-            int4 tdn = s_task[warp];  // the next task's descriptor, loaded one task ahead
-            // the task loop is unrolled (acc[t] register-indexed) only while the code stays
-            // small; otherwise each task's block sum is added to acc[t] by predicated adds
-            constexpr bool kUnrollT = R * kMaxT <= 64;
-#pragma unroll(kUnrollT ? kMaxT : 1)
-            for (int t = 0; t < kMaxT; ++t) {
-                const int4 td = tdn;  // warp-uniform (broadcast)
-                const int k = td.x;
-                if (k < 0) break;
-                const int4 ent = btab[k * nbu + i];
-                if (t + 1 < kMaxT) tdn = s_task[warp + kWarps * (t + 1)];
-                if (td.y > ent.w || td.y + kChunk - 1 < ent.z) continue;  // chunk misses the block
-#ifdef SKEI_FWD_STATS
-                const long long tt0 = clock64();
-                ++st_active;
-                st_lanes += max(0, min(td.y + kChunk - 1, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
-#endif
+            // one task's line loop over the staged block: lo / hi = the block's sums of the
+            // lane's lower / upper bin (shared by the warps' own tasks and the floating ones)
+            auto task_block = [&](const int4 td, const int4 ent, const int k, float (&lo)[BB],
+                                  float (&hi)[BB]) {
                 int base = ent.x + td.z;
                 float frac = __int_as_float(ent.y) + __int_as_float(td.w);
                 if (frac >= 1.f) {
@@ -715,7 +737,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 for (int b = 0; b < LB; ++b) d[b] = sgn[b] * plf;
                 const unsigned pbase = cur_b + lofs0;  // bits 0..6 = line lane'
                 float e = fmaf(lf0, plf, fs);
-                float lo[BB], hi[BB];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) lo[b] = hi[b] = 0.f;
                 // the line loop, compiled twice: with and without the fifth candidate (wide is
@@ -824,6 +845,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
 #else
                 run_lines(std::true_type{});
 #endif
+            };
+            int4 tdn = s_task[warp];  // the next task's descriptor, loaded one task ahead
+            // the task loop is unrolled (acc[t] register-indexed) only while the code stays
+            // small; otherwise each task's block sum is added to acc[t] by predicated adds
+            constexpr bool kUnrollT = R * kMaxT <= 64;
+#pragma unroll(kUnrollT ? kMaxT : 1)
+            for (int t = 0; t < kMaxT; ++t) {
+                const int4 td = tdn;  // warp-uniform (broadcast)
+                const int k = td.x;
+                if (k < 0) break;
+                const int4 ent = btab[k * nbu + i];
+                if (t + 1 < kMaxT) tdn = s_task[warp + kWarps * (t + 1)];
+                if (td.y > ent.w || td.y + kChunk - 1 < ent.z) continue;  // chunk misses the block
+#ifdef SKEI_FWD_STATS
+                const long long tt0 = clock64();
+                ++st_active;
+                st_lanes += max(0, min(td.y + kChunk - 1, min(ent.w, n_det - 1)) - max(td.y, ent.z) + 1);
+#endif
+                float lo[BB], hi[BB];
+                task_block(td, ent, k, lo, hi);
 #ifdef SKEI_FWD_STATS
 #pragma unroll
                 for (int tt = 0; tt < kMaxT; ++tt)
@@ -850,6 +891,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                         }
                 }
             }
+            // floating tasks: a warp done with its own tasks of this block takes the block's
+            // floating tasks from a shared queue until none is left (each warp's last grab
+            // fails, so a block adds nfl + kWarps to its buffer's counter).  The block sums are
+            // added to the task's shared-memory sums in block order (s_fseq; a chunk's blocks
+            // are consecutive, and block i's queue opens only after block i - 1's is empty, so
+            // the sum a warp waits for is already being computed): the result is bitwise the
+            // one a warp-owned task gives.
+            if constexpr (kFloat) {
+                if (nfl > 0) {
+                    const int fbase = (nfl + kWarps) * (i / nbuf);
+                    for (;;) {
+                        int f = 0;
+                        if (lane == 0) f = atomicAdd(&s_fq[cb], 1) - fbase;
+                        f = __shfl_sync(0xffffffffu, f, 0);
+                        if (f >= nfl) break;
+                        const int4 td = s_float[f];
+                        const int k = td.x;
+                        const int4 ent = btab[k * nbu + i];
+                        if (td.y > ent.w || td.y + kChunk - 1 < ent.z) continue;
+#ifdef SKEI_FWD_STATS
+                        ++st_active;
+                        ++st_fl;
+#endif
+                        float lo[BB], hi[BB];
+                        task_block(td, ent, k, lo, hi);
+                        bool first = i == 0;
+                        if (!first) {
+                            const int4 pe = btab[k * nbu + i - 1];
+                            first = td.y > pe.w || td.y + kChunk - 1 < pe.z;
+                        }
+                        float4 *fa = reinterpret_cast<float4 *>(facc) + (size_t)f * 64 + lane;
+                        float4 alo = make_float4(0.f, 0.f, 0.f, 0.f), ahi = alo;
+                        if (!first) {
+                            if (lane == 0) {
+                                while (*reinterpret_cast<volatile int *>(&s_fseq[f]) != i) {
+                                }
+                                __threadfence_block();
+                            }
+                            __syncwarp();
+                            alo = fa[0];
+                            ahi = fa[32];
+                        }
+                        alo.x += lo[0], alo.y += lo[1], alo.z += lo[2], alo.w += lo[3];
+                        ahi.x += hi[0], ahi.y += hi[1], ahi.z += hi[2], ahi.w += hi[3];
+                        fa[0] = alo;
+                        fa[32] = ahi;
+                        __syncwarp();
+                        if (lane == 0) {
+                            __threadfence_block();
+                            *reinterpret_cast<volatile int *>(&s_fseq[f]) = i + 1;
+                        }
+                    }
+                }
+            }
             // release the buffer; the last warp out refills it with block g + nbuf
             __syncwarp();
             if (lane == 0) {
@@ -862,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
             }
         }
 
-#ifdef SKEI_FWD_STATS
+#if defined(SKEI_FWD_STATS) && defined(SKEI_FWD_STATS_TASKS)
         if (lane == 0 && (blockIdx.x % SKEI_FWD_STATS_EVERY) == 0) {
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
@@ -874,6 +969,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 st_tn[t] = st_tc[t] = 0;
             }
         }
+#endif
+#ifdef SKEI_FWD_STATS
         const long long te0 = clock64();
 #endif
         // ---- 4. unit epilogue.  A whole unit is complete in this CTA's registers: each lane
@@ -920,6 +1017,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 s1[b] = neg ? acc[t][b] : acc[t][BB + b];
             }
         };
+        // the same for floating task f (angle slot k): its sums are in shared memory
+        auto float_sums = [&](int f, int k, float (&s0)[BB], float (&s1)[BB]) {
+            const bool neg = sAngT[k][0].w < 0.f;
+            const float *fa = facc + ((size_t)f * 64 + lane) * 4;
+#pragma unroll
+            for (int b = 0; b < BB; ++b) {
+                const float l = fa[b < 4 ? b : 0], h = fa[128 + (b < 4 ? b : 0)];
+                s0[b] = neg ? h : l;
+                s1[b] = neg ? l : h;
+            }
+        };
         if (full_unit) {
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
@@ -936,6 +1044,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 const int k = tau / a.chunks, j = (tau - k * a.chunks) * kChunk + 2 * lane;
                 if (j < n_det) finish_bin(sSlot[k], j, zero);
                 if (j + 1 < n_det) finish_bin(sSlot[k], j + 1, zero);
+            }
+            if constexpr (kFloat) {
+                if (nfl > 0) {
+                    __syncthreads();  // every floating task's sums complete
+                    if (warp < nfl) {
+                        const int4 td = s_float[warp];
+                        const int j = td.y + 2 * lane;
+                        float s0[BB], s1[BB];
+                        float_sums(warp, td.x, s0, s1);
+                        if (j < n_det) finish_bin(sSlot[td.x], j, s0);
+                        if (j + 1 < n_det) finish_bin(sSlot[td.x], j + 1, s1);
+                    }
+                }
             }
         } else {
             float *mine = pieces + ((long)cid * 2 + (u == u_first ? 0 : 1)) * part_f;
@@ -954,6 +1075,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                 const int k = tau / a.chunks, j = (tau - k * a.chunks) * kChunk + 2 * lane;
                 if (j < n_det) stg_vec<BB>(mine + ((long)k * n_det + j) * BB, zero);
                 if (j + 1 < n_det) stg_vec<BB>(mine + ((long)k * n_det + j + 1) * BB, zero);
+            }
+            if constexpr (kFloat) {
+                if (nfl > 0) {
+                    __syncthreads();  // every floating task's sums complete
+                    if (warp < nfl) {
+                        const int4 td = s_float[warp];
+                        const int j = td.y + 2 * lane;
+                        float s0[BB], s1[BB];
+                        float_sums(warp, td.x, s0, s1);
+                        if (j < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j) * BB, s0);
+                        if (j + 1 < n_det) stg_vec<BB>(mine + ((long)td.x * n_det + j + 1) * BB, s1);
+                    }
+                }
             }
             __threadfence();
             __syncthreads();  // the whole piece written (and fenced)
@@ -1122,7 +1256,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
     if (lane == 0 && (blockIdx.x % SKEI_FWD_STATS_EVERY) == 0)
         printf("FWDSTAT cta %d warp %d units %d G %d wait %lld pro %lld epi %lld total %lld active %lld "
                "lanes %lld esync %lld fin %lld\n", blockIdx.x, warp, u_last - u_first + 1, G, st_wait,
-               st_pro, st_epi, clock64() - st_t0, st_active, st_lanes, 0LL, st_fin);
+               st_pro, st_epi, clock64() - st_t0, st_active, st_lanes, st_fl, st_fin);
 #endif
     // ---- 5. MC residual final: the last CTA sums each image's (unit, rank) partials in order
     if (!a.job[0].y) return;
@@ -1187,8 +1321,15 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     }
     const size_t limit = (size_t)limit_i;
     a.nbuf = 3 * stage_b + tab_b <= limit ? 3 : (2 * stage_b + tab_b <= limit ? 2 : 1);
-    const size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
+    size_t smem = a.nbuf * stage_b + tab_b + 128;  // + alignment slack
     if (smem > limit) return cudaErrorInvalidValue;
+    // floating tasks (groups of 4): as many as the shared memory left over holds
+    a.nfloat = 0;
+    if (BB == 4 && !FUSED && kMaxFloat > 0) {
+        const size_t room = (limit - smem) / kFloatBytes;
+        a.nfloat = room < (size_t)kMaxFloat ? (int)room : kMaxFloat;
+        smem += (size_t)a.nfloat * kFloatBytes;
+    }
     if (num_sms > kMaxPieces || num_sms > kPassCounters - 2) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)num_sms, 1, 1);
