@@ -87,6 +87,7 @@ constexpr int kMaxTaskBB = cmax_(cmax_(4 * max_tasks<4>(), 2 * max_tasks<2>()), 
 constexpr int kMinTasks = max_tasks<4>() < max_tasks<2>() ? max_tasks<4>() : max_tasks<2>();
 static_assert(kMinTasks <= max_tasks<1>(), "");
 constexpr int kKMax = 16;   // angles per CTA
+constexpr int kSmallK = 3, kSmallBlocks = 8;  // small problems: see launch_bb
 #ifndef SKEI_FWD_AHEAD
 #define SKEI_FWD_AHEAD 1
 #endif
@@ -132,6 +133,9 @@ constexpr int kMaxBand = 64;     // band angles of the source class considered f
 // of the static deal is time in which the other warps run faster, not idle capacity.
 #ifndef SKEI_FWD_FLOAT
 #define SKEI_FWD_FLOAT 0
+#endif
+#ifndef SKEI_FWD_LANE_SKIP
+#define SKEI_FWD_LANE_SKIP 0  // A/B knob: lanes outside the block's bin range skip the line loop
 #endif
 constexpr int kMaxFloat = SKEI_FWD_FLOAT < kWarps ? SKEI_FWD_FLOAT : kWarps;
 constexpr int kFloatBytes = 32 * 2 * 4 * (int)sizeof(float);  // a floating task's sums (BB = 4)
@@ -837,6 +841,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_radon_fwd(const __grid_constant
                     use_line(v[cur], ph[cur]);
                 }
                 };
+#if SKEI_FWD_LANE_SKIP
+                // lanes whose bin pair no line of the block can see skip the line loop (their
+                // sums stay 0): a quarter-warp of such lanes issues no shared-memory wavefronts
+                const int jlane = td.y + 2 * lane;
+                if (jlane + 1 < ent.z || jlane > ent.w) return;
+#endif
 #if SKEI_FWD_WIDE_SPLIT
                 if (wide)
                     run_lines(std::true_type{});
@@ -1284,9 +1294,25 @@ cudaError_t launch_bb(FwdArgs a, int num_sms, cudaStream_t s) {
     a.K = (kWarps * max_tasks<BB>()) / a.chunks;
     if (a.K > kKMax) a.K = kKMax;
     if (a.K < 1) return cudaErrorInvalidValue;  // n_det > kWarps * kMaxT * kChunk
+#ifdef SKEI_FWD_KCAP_ENV
+    if (const char *kc = std::getenv("SKEI_FWD_KCAP")) {
+        const int cap = std::atoi(kc);
+        if (cap >= 1 && cap < a.K) a.K = cap;
+    }
+#endif
     a.nblk = (a.g.n + R - 1) / R;
     a.nq = a.fused ? a.B : a.B / BB;
     if (a.nq > kMaxQ) return cudaErrorInvalidValue;
+    // Small problems (fewer than kSmallBlocks line blocks per CTA at the largest K): units of
+    // at most kSmallK angles, so the work spreads over angles as well as line blocks — a
+    // CTA's per-unit prologue and its split-unit piece shrink with K, and a unit is cut into
+    // fewer pieces.  Measured (round 2, fifth session): cfg2 forward 60.6 -> 50.0 us (K 10 ->
+    // 3; K = 2: 51.3, K = 1: 63.8), cfg1 41.1 -> 36.1 us; cfg5 (22 blocks per CTA) gets slower
+    // with any smaller K (249.6 us at K = 5, 265.8 at 3) and keeps the largest.
+    {
+        const long units = ((long)a.njobs * a.nq * a.m + a.K - 1) / a.K;
+        if (units * a.nblk < (long)kSmallBlocks * num_sms && a.K > kSmallK) a.K = kSmallK;
+    }
     const size_t stage_b = sizeof(float) * (size_t)(a.g.n + kPadL + kPadR) * kColF;
     const size_t tab_b = sizeof(int4) * (size_t)a.K * a.nblk;  // block table (any S)
     // dynamic shared memory budget: 227 KB per CTA less the static tables.  The function
@@ -1407,6 +1433,10 @@ size_t fwd_mc_slots(const skei_plan *plan, int B, int m, int idx_stride) {
     int K = (kWarps * kMinTasks) / chunks;  // the smallest K over the group sizes BB
     if (K > kKMax) K = kKMax;
     if (K < 1) K = 1;
+    if (K > kSmallK) K = kSmallK;  // small problems run with K <= kSmallK (launch_bb)
+#ifdef SKEI_FWD_KCAP_ENV
+    K = 1;
+#endif
     return (size_t)((m + K - 1) / K + 2);  // units per image group
 }
 
