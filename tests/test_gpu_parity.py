@@ -112,6 +112,28 @@ def test_radon_fwd_parity(geom):
         close(p[b], oracle.fwd(x[b], idxs[b], n_full, n_det), f"fwd per-image b={b}")
 
 
+def test_radon_fwd_small_problem_units_both_sides_of_the_rule():
+    """The forward runs small launches (fewer than 8 line blocks per CTA) with at most 3
+    angles per unit and larger ones with the largest K (radon_fwd.cu, launch_bb).  Same
+    geometry (cfg2's: 256 px, 363 bins, 32 of 128 angles) on both sides of the rule: a batch
+    of 4 (3-angle units) and a batch of 64 whose first 4 images are the same (10-angle
+    units).  Both against the oracle; against each other the projections agree to fp32
+    rounding (a split unit's pieces are cut elsewhere, and the flexible class band moves
+    other near-diagonal angles between the row and the column class when K changes)."""
+    N, n_det, n_full, P, m = 256, 363, 128, 1024, 32
+    plan = _plan(N, n_det, n_full, P)
+    xs = synth.rand_images(4, N, 11)
+    idx = _draw_list(n_full, m, seed=9)
+    ref = oracle.fwd(xs, idx, n_full, n_det)
+    p_small = sk.radon_fwd(plan, dev(xs), idx_t(idx))
+    close(p_small, ref, "fwd small launch")
+    xl = np.concatenate([xs] * 16, axis=0)
+    p_large = sk.radon_fwd(plan, dev(xl), idx_t(idx))
+    close(p_large[:4], ref, "fwd large launch, images 0..3")
+    close(p_large[60:], ref, "fwd large launch, images 60..63")
+    close(p_large[:4], p_small.double().cpu().numpy(), "large vs small launch", tol=2e-5)
+
+
 @pytest.mark.parametrize("geom", GEOMS)
 def test_radon_adj_parity(geom):
     N, n_det, n_full, P, B, m = geom
