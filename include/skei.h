@@ -316,9 +316,14 @@ skei_status skei_pass(const skei_plan *plan, int32_t B, const float *x1, const f
 /* End-to-end variant from HOST buffers: copies host x1 [B][n][n], host y
  * [B][n_full][n_det], host g [B or 1] and host idx into the caller's device
  * buffers (d_x1, d_y, d_g, d_idx, same shapes), runs skei_pass, and copies
- * mc/ei back into host h_mc[B], h_ei[B].  If h_ystage (host, >= B*m*n_det floats,
- * pinned) is given, only the m sketched rows of each image's y cross the link (the
- * pass only reads y_S, Alg. 1 step 6): image b's rows idx_b[0..m) (its own sketch when
+ * mc/ei back into host h_mc[B], h_ei[B].  Only the m sketched rows of each image's y
+ * need to cross the link (the pass only reads y_S, Alg. 1 step 6).  Equispaced
+ * sketches (uniform mode: idx_b[k] = idx_b[0] + k d; for a shared sketch also d | n_full)
+ * are copied in place as a pitched sub-array of y — one 3-D copy for a shared sketch,
+ * one 2-D copy per image otherwise — into the head of d_y as y_S [B][m][n_det], with no
+ * host gather and h_ystage untouched (transfers under 2 MB with an h_ystage keep the
+ * gather: it is cheaper than the pitched copy's per-row cost).  Otherwise, if h_ystage (host, >= B*m*n_det floats,
+ * pinned) is given: image b's rows idx_b[0..m) (its own sketch when
  * idx_stride = m) are gathered into it on the calling thread (up to 8 host threads for
  * batches over 4 MB of rows) and sent as one copy into the head of d_y as y_S
  * [B][m][n_det].  h_ystage is rewritten at call time, so a previous call's copy from it
