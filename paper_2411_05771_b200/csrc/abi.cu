@@ -820,6 +820,8 @@ skei_status skei_pass_host(const skei_plan *plan, int32_t B, const float *h_x1,
     // copy's per-row cost on the copy engine outweighs a 30 us gather — e2e 6700 vs 3800
     // passes/s; cfg3, 4.2 MB: host enqueue 0.34 -> 0.05 ms per step at the same step time)
     if (h_ystage && sizeof(float) * (size_t)B * m * n_det < ((size_t)2 << 20)) pitched = false;
+    if (const char *e = std::getenv("SKEI_HOST_PITCHED"))  // A/B knob: 0 = always gather
+        if (e[0] == '0') pitched = false;
     const bool y_sk = idx_stride == 0 || h_ystage || pitched;
     if (pitched && idx_stride == 0) {
         const int d = stride_of(h_idx);
