@@ -853,7 +853,7 @@ def main():
                 el = float(t.item())
             reps.append(el)
         el = float(np.median(reps))
-        # only each image's m sketched rows of y cross the link (skei_pass_host gathers them)
+        # only each image's m sketched rows of y cross the link (skei_pass_host: pitched copy or gather)
         y_h2d = B * m * cfg.n_det * 4
         h2d = hx1.numel() * 4 + y_h2d + ng * 4 + ng * m * 4
         d2h = 2 * B * 4 + (B * N * N * 4 if args.e2e_grad else 0)
@@ -864,8 +864,10 @@ def main():
                           "mc, ei (the gradient and x_fbp stay on the device; --e2e-grad reads "
                           "the gradient back too)",
                "timing": "host wall clock over all steps; per step: host draw, H2D of x1, y_S "
-                         "(the sketched rows of y gathered into a pinned staging buffer by the "
-                         "library, each image's own rows for per-image sketches), g, idx "
+                         "(the sketched rows of y: an equispaced sketch's rows are copied in place "
+                         "as a pitched sub-array of y, a random sketch's are gathered into a pinned "
+                         "staging buffer by the library; each image's own rows for per-image "
+                         "sketches), g, idx "
                          "from pinned memory, the pass, D2H of its results, in-stream L2 flush "
                          "(256 MB write) behind it; slots with their own streams rotate, so one "
                          "step's H2D overlaps the previous steps' passes (3 slots); the median "
